@@ -1,0 +1,154 @@
+"""FireCaffe CPU oracle — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (the
+``cpu_baseline`` leg and ``--impl reference``) may import this package.  The
+product package ``paper_1511_00175_b200`` never imports it, and it imports
+nothing from the product package: the two share no code.
+
+The arithmetic lives in ``oracle.cpp`` (plain single-threaded C++, fp32 with
+explicit ``std::fma``, ``-ffp-contract=off``); this module only builds it with
+gcc and marshals numpy arrays through ctypes.  ``comm_model.py`` holds the
+paper's closed-form communication-time models (Eq. 3 and Eq. 4).
+
+Parity status of each function (DESIGN.md §3 lists the pins):
+  tree_sum   pinned: brute-force expression trees (P1), integer exactness (P2),
+             SPEC S:382 vector (P3), pairwise-summation error bound (P5).
+  ps_sum     pinned: sequential expression (P1), == tree_sum(k=p), P2, P3.
+  sgd        pinned: SPEC S:89-91 worked examples (P4), float64 rule (A15),
+             torch.optim.SGD equivalence within tolerance (P6).
+  sum_f64 / sgd_f64: float64 references; pinned by exact integer cases and
+             math.fsum.
+  comm_model pinned: SPEC S:272-282 / S:308 closed-form values (P7).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.cpp -> liboracle.so with gcc (no GPU, no CUDA)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call(["g++", *CFLAGS, "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P, I, I64, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
+        L.oracle_version.restype = I
+        L.oracle_tree_sum.argtypes = [P, I, I64, I, P]
+        L.oracle_ps_sum.argtypes = [P, I, I64, P]
+        L.oracle_sgd.argtypes = [P, P, P, I64, F, F, F, I64]
+        L.oracle_sum_f64.argtypes = [P, I, I64, P]
+        L.oracle_abs_sum_f64.argtypes = [P, I, I64, P]
+        L.oracle_sgd_f64.argtypes = [P, P, P, I64, F, F, F, I64]
+        L.oracle_tree_plan.argtypes = [I, I, P, I]
+        for f in ("oracle_tree_sum", "oracle_ps_sum", "oracle_sgd", "oracle_sum_f64",
+                  "oracle_abs_sum_f64", "oracle_sgd_f64", "oracle_tree_plan"):
+            getattr(L, f).restype = I
+        _lib = L
+    return _lib
+
+
+def _f32(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    return a
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise ValueError(f"oracle {what}: invalid arguments (rc={rc})")
+
+
+def tree_sum(g, k: int = 2) -> np.ndarray:
+    """Reduction-tree sum of g[p, n] with branching factor k."""
+    g = _f32(g)
+    p, n = g.shape
+    out = np.empty(n, np.float32)
+    _check(lib().oracle_tree_sum(_ptr(g), p, n, k, _ptr(out)), "tree_sum")
+    return out
+
+
+def ps_sum(g) -> np.ndarray:
+    """Parameter-server sum, ascending rank."""
+    g = _f32(g)
+    p, n = g.shape
+    out = np.empty(n, np.float32)
+    _check(lib().oracle_ps_sum(_ptr(g), p, n, _ptr(out)), "ps_sum")
+    return out
+
+
+def sgd(w, v, S, lr: float, mu: float, wd: float, batch: int):
+    """One Caffe-convention SGD step; returns new (w', v') arrays."""
+    w = _f32(w).copy()
+    v = _f32(v).copy()
+    S = _f32(S)
+    n = w.shape[0]
+    assert v.shape == (n,) and S.shape == (n,)
+    _check(lib().oracle_sgd(_ptr(w), _ptr(v), _ptr(S), n, lr, mu, wd, batch), "sgd")
+    return w, v
+
+
+def sum_f64(g) -> np.ndarray:
+    """float64 left-to-right sum over ranks."""
+    g = _f32(g)
+    p, n = g.shape
+    out = np.empty(n, np.float64)
+    _check(lib().oracle_sum_f64(_ptr(g), p, n, _ptr(out)), "sum_f64")
+    return out
+
+
+def abs_sum_f64(g) -> np.ndarray:
+    g = _f32(g)
+    p, n = g.shape
+    out = np.empty(n, np.float64)
+    _check(lib().oracle_abs_sum_f64(_ptr(g), p, n, _ptr(out)), "abs_sum_f64")
+    return out
+
+
+def sgd_f64(w64, v64, S64, lr: float, mu: float, wd: float, batch: int):
+    w64 = np.ascontiguousarray(w64, dtype=np.float64).copy()
+    v64 = np.ascontiguousarray(v64, dtype=np.float64).copy()
+    S64 = np.ascontiguousarray(S64, dtype=np.float64)
+    n = w64.shape[0]
+    _check(lib().oracle_sgd_f64(_ptr(w64), _ptr(v64), _ptr(S64), n, lr, mu, wd, batch), "sgd_f64")
+    return w64, v64
+
+
+def tree_plan(p: int, k: int = 2):
+    """Reduce-phase edges [(level, sender, receiver), ...]."""
+    L = lib()
+    m = L.oracle_tree_plan(p, k, None, 0)
+    if m < 0:
+        raise ValueError("tree_plan: invalid arguments")
+    buf = (ctypes.c_int * max(1, 3 * m))()
+    L.oracle_tree_plan(p, k, ctypes.cast(buf, ctypes.c_void_p), m)
+    return [(buf[3 * e], buf[3 * e + 1], buf[3 * e + 2]) for e in range(m)]
+
+
+def fused_step(g, w, v, lr: float, mu: float, wd: float, batch: int, k: int = 2):
+    """The whole hot path for one iteration: tree sum, then one SGD step
+    (the sum is what a single GPU would compute; P:121 update).
+    Every rank ends with the same (w', v')."""
+    S = tree_sum(g, k)
+    return sgd(w, v, S, lr, mu, wd, batch)

@@ -1,0 +1,200 @@
+// FireCaffe CPU oracle — TEST INFRASTRUCTURE ONLY.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py (its cpu_baseline leg and
+// `--impl reference`) may load this library. The product path
+// (paper_1511_00175_b200/) never links, imports or calls it, and this file
+// shares no code, header, constant or helper with the CUDA path.
+//
+// Plain, slow, obviously-correct host C++ of what the data-parallel hot path
+// computes (PAPER.md = /root/reference/PAPER.md, cited as P:line):
+//
+//   * oracle_tree_sum  — element-wise sum of the p per-worker gradient vectors
+//     through a k-nomial reduction tree rooted at rank 0 (§6.2
+//     "binomial reduction tree", Fig. P:312-315).  The floating-point
+//     association is the tree's own (reading R1): at step s = k^l,
+//     node r (r mod k·s == 0) absorbs r + j·s for j = 1..k-1 in ascending order.
+//   * oracle_ps_sum    — the parameter server of §6.1:
+//     one node sums every worker's gradient, ascending rank, sequentially
+//     (the tree of height 1 and branching factor p).  Reading R4.
+//   * oracle_sgd       — one SGD step with momentum and weight decay
+//     (rule not written in the paper -> Caffe convention,
+//     reading R6): g = S·fl(1/B) (inputs are per-worker SUMS of ∇W, P:235-236,
+//     reading R7), d = fma(wd, w, g), v' = fma(mu, v, fl(lr·d)), w' = w − v'.
+//   * oracle_sum_f64 / oracle_sgd_f64 — float64 left-to-right references used
+//     for the "1e-6 relative vs float64" tolerance in north_star.
+//
+// Build: g++ -O2 -std=c++17 -ffp-contract=off -fno-fast-math -shared -fPIC.
+// -ffp-contract=off matters: a contracted a*b+c would change the rounding
+// sequence the oracle defines.  std::fma is a true fused multiply-add
+// (one rounding), emulation through double is NOT (SURVEY.md §0 finding 6).
+// x86-64 evaluates float arithmetic in float (SSE, FLT_EVAL_METHOD == 0), so
+// every `+`, `*`, `-` below is one IEEE round-to-nearest-even fp32 operation.
+// Everything is single-threaded, no FTZ/DAZ (MXCSR default).
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+extern "C" {
+
+// Version tag so tests can check they loaded the intended build.
+int oracle_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// Reduction tree sum (Eq. 4; Fig. P:312-315).
+//
+// g   : p*n floats, row-major (g[r*n + i] = worker r's gradient element i)
+// out : n floats, the tree's root value (what every rank ends with after the
+//       broadcast "back down the tree").
+// k   : branching factor, 2 <= k; k >= p gives the one-level tree = PS order.
+//
+// Per element i (elements are independent, "element-wise addition"):
+//   part[r] = g[r][i]
+//   step = 1
+//   while step < p:
+//     for r = 0, k*step, 2*k*step, ... < p:
+//       for j = 1 .. k-1:                  (children in ascending rank)
+//         c = r + j*step
+//         if c < p: part[r] = fl32(part[r] + part[c])
+//     step *= k
+//   out[i] = part[0]
+// ---------------------------------------------------------------------------
+int oracle_tree_sum(const float* g, int p, int64_t n, int k, float* out) {
+    if (p < 1 || n < 0 || k < 2 || (n > 0 && (!g || !out))) return 1;
+    std::vector<float> part((size_t)p);
+    for (int64_t i = 0; i < n; ++i) {
+        for (int r = 0; r < p; ++r) part[(size_t)r] = g[(int64_t)r * n + i];
+        int64_t step = 1;
+        while (step < p) {
+            for (int64_t r = 0; r < p; r += (int64_t)k * step) {
+                for (int j = 1; j <= k - 1; ++j) {
+                    int64_t c = r + (int64_t)j * step;
+                    if (c < p) {
+                        part[(size_t)r] = part[(size_t)r] + part[(size_t)c];
+                    }
+                }
+            }
+            step *= k;
+        }
+        out[i] = part[0];
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Parameter-server sum: the server adds the workers'
+// gradients one after another, ascending rank: ((g0+g1)+g2)+...+g_{p-1}.
+// Written out on its own (not by calling the tree with k=p) so that the
+// "k=p tree == PS" identity is a test, not a tautology.
+// ---------------------------------------------------------------------------
+int oracle_ps_sum(const float* g, int p, int64_t n, float* out) {
+    if (p < 1 || n < 0 || (n > 0 && (!g || !out))) return 1;
+    for (int64_t i = 0; i < n; ++i) {
+        float acc = g[i];
+        for (int r = 1; r < p; ++r) {
+            acc = acc + g[(int64_t)r * n + i];
+        }
+        out[i] = acc;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// SGD with momentum and weight decay, in place (μ, wd P:358, P:363;
+// lr P:413; Caffe convention per SPEC S:86 and reading R6).
+//   inv_b = fl32(1 / (float)B)          (global batch B, reading R7)
+//   g  = fl32(S · inv_b)
+//   d  = fma(wd, w, g)                  (g + wd·w, one rounding)
+//   t  = fl32(lr · d)
+//   v' = fma(mu, v, t)                  (mu·v + lr·d, one rounding)
+//   w' = fl32(w − v')
+// ---------------------------------------------------------------------------
+int oracle_sgd(float* w, float* v, const float* S, int64_t n, float lr, float mu,
+               float wd, int64_t batch) {
+    if (n < 0 || batch < 1 || (n > 0 && (!w || !v || !S))) return 1;
+    const float inv_b = 1.0f / (float)batch;
+    for (int64_t i = 0; i < n; ++i) {
+        const float g = S[i] * inv_b;
+        const float d = std::fma(wd, w[i], g);
+        const float t = lr * d;
+        const float vn = std::fma(mu, v[i], t);
+        const float wn = w[i] - vn;
+        v[i] = vn;
+        w[i] = wn;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// float64 references (north_star: "within 1e-6 relative error (fp32) against
+// a naive left-to-right float64 sum").
+// ---------------------------------------------------------------------------
+int oracle_sum_f64(const float* g, int p, int64_t n, double* out) {
+    if (p < 1 || n < 0 || (n > 0 && (!g || !out))) return 1;
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int r = 0; r < p; ++r) acc += (double)g[(int64_t)r * n + i];
+        out[i] = acc;
+    }
+    return 0;
+}
+
+// Σ_r |g_r[i]| in float64: the scale the summation error bound is stated in.
+int oracle_abs_sum_f64(const float* g, int p, int64_t n, double* out) {
+    if (p < 1 || n < 0 || (n > 0 && (!g || !out))) return 1;
+    for (int64_t i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int r = 0; r < p; ++r) acc += std::fabs((double)g[(int64_t)r * n + i]);
+        out[i] = acc;
+    }
+    return 0;
+}
+
+// Same SGD rule in float64 (fp32 hyper-parameters promoted); S64 is the
+// float64 gradient sum.  w64, v64 are in/out.
+int oracle_sgd_f64(double* w64, double* v64, const double* S64, int64_t n, float lr,
+                   float mu, float wd, int64_t batch) {
+    if (n < 0 || batch < 1 || (n > 0 && (!w64 || !v64 || !S64))) return 1;
+    for (int64_t i = 0; i < n; ++i) {
+        double g = S64[i] / (double)batch;
+        double d = g + (double)wd * w64[i];
+        double vn = (double)mu * v64[i] + (double)lr * d;
+        v64[i] = vn;
+        w64[i] = w64[i] - vn;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// The reduce phase of the tree as a communication plan (SPEC S:367-375
+// `plan_topology`): every (level, sender -> receiver) edge in the
+// order the oracle's loop visits them.  Returns the number of edges written
+// (at most cap); edges[3*e+0..2] = level, sender (child), receiver (parent).
+// ---------------------------------------------------------------------------
+int oracle_tree_plan(int p, int k, int* edges, int cap) {
+    if (p < 1 || k < 2) return -1;
+    int e = 0;
+    int level = 0;
+    int64_t step = 1;
+    while (step < p) {
+        for (int64_t r = 0; r < p; r += (int64_t)k * step) {
+            for (int j = 1; j <= k - 1; ++j) {
+                int64_t c = r + (int64_t)j * step;
+                if (c < p) {
+                    if (e < cap && edges) {
+                        edges[3 * e + 0] = level;
+                        edges[3 * e + 1] = (int)c;
+                        edges[3 * e + 2] = (int)r;
+                    }
+                    ++e;
+                }
+            }
+        }
+        step *= k;
+        ++level;
+    }
+    return e;
+}
+
+}  // extern "C"
