@@ -1,0 +1,214 @@
+/* firecaffe.h — C ABI of the B200-native FireCaffe data-parallel hot path.
+ *
+ * FireCaffe (Iandola et al., arXiv 1511.00175; PAPER.md = the paper's text,
+ * cited as P:line) trains with data parallelism: every worker computes the SUM
+ * of the weight gradients over its part of the batch, the
+ * per-worker sums are added across workers ("identical numerical
+ * results as ... a single GPU") through a reduction tree (§6.2,
+ * P:276-303) instead of a parameter server (§6.1), the sums go
+ * "back down the tree", and every replica applies the SGD update
+ * with momentum and weight decay.
+ *
+ * This library implements that per-iteration aggregation + update for one
+ * NVSwitch node of B200 GPUs (1..8 ranks, one process per GPU):
+ *   firecaffe_sgd_step            1-GPU fused SGD (the update alone)
+ *   firecaffe_tree_allreduce      reduction-tree sum, result on every rank
+ *   firecaffe_tree_allreduce_sgd  tree sum fused with the SGD update at each
+ *                                 subtree root + broadcast of the new weights
+ *   firecaffe_ps_allreduce        the paper's parameter server (baseline)
+ *
+ * Conventions (all functions):
+ *   - All float buffers are fp32, in DEVICE memory, 16-byte aligned, and must
+ *     not overlap.  The caller owns all memory; the library allocates device
+ *     memory only in firecaffe_heap_alloc / firecaffe_world_create*.
+ *   - Calls that take a `stream` (a cudaStream_t, passed as void*) are
+ *     asynchronous: they validate on the host, enqueue one kernel and return.
+ *     Host-detectable errors are returned synchronously and nothing is
+ *     enqueued.  Device-side errors (a peer that never arrives) are sticky and
+ *     returned by firecaffe_world_poll.
+ *   - Collective calls (tree_*, ps_*) must be issued by every rank of the
+ *     world in the same order with the same n and hyper-parameters (the
+ *     MPI/NCCL convention).  Their `grad`, `w` (and, for a virtual world,
+ *     `mom`) must lie inside the world's heap at the SAME byte offset on every
+ *     rank (symmetric allocation), at or after firecaffe_heap_reserved_bytes().
+ *   - Numerics: round-to-nearest-even fp32, no FTZ, no fast-math; the summation
+ *     association is fixed (documented per call) so results are bitwise
+ *     deterministic and identical on every rank.  Inputs must be
+ *     finite (NaN payloads are not reproducible across CPU/GPU).
+ */
+#ifndef FIRECAFFE_H
+#define FIRECAFFE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FC_OK = 0,
+    FC_ERR_INVALID_ARG = 1,   /* null/misaligned pointer, n < 0, lr <= 0, mu not in [0,1), wd < 0, batch < 1, overlap */
+    FC_ERR_NOT_SYMMETRIC = 2, /* a collective buffer is outside the heap or inside its reserved prefix */
+    FC_ERR_MISMATCH = 3,      /* world/device mismatch (e.g. called on another device) */
+    FC_ERR_TIMEOUT = 4,       /* a peer did not arrive within the world's timeout (sticky) */
+    FC_ERR_CUDA = 5,          /* a CUDA runtime call failed */
+    FC_ERR_UNSUPPORTED = 6    /* schedule/arity not available for this world size */
+} fc_status;
+
+/* Who executes the reduction tree.  The VALUE never depends on it: every
+ * schedule computes the same k-nomial association (see firecaffe_tree_allreduce). */
+typedef enum {
+    FC_SCHED_FOREST = 0,      /* XOR-rotated binomial forest: p owner slices, slice s reduced by a
+                                 binomial tree rooted at rank s; level l pulls |W|/2^(l+1) from rank
+                                 r^2^l over NVLink (recursive halving).  p power of two, arity 2. */
+    FC_SCHED_SINGLE_ROOT = 1, /* the paper's single binomial tree rooted at rank 0 (Fig. P:312-315):
+                                 level l, rank r (r mod 2^(l+1) == 0) pulls all of |W| from r+2^l. arity 2 */
+    FC_SCHED_FLAT = 2         /* every rank pulls its owner slice from all p-1 peers at once and evaluates
+                                 the tree in registers (one communication level); any p, any arity */
+} fc_sched;
+
+/* How the result goes "back down the tree". Bytes only: value-neutral. */
+typedef enum {
+    FC_BCAST_TREE = 0,        /* mirror of the reduce levels (recursive doubling for the forest) */
+    FC_BCAST_DIRECT = 1       /* each owner pushes its slice to every peer in one level */
+} fc_bcast;
+
+typedef struct fc_world fc_world; /* opaque; one per process (or one per virtual world) */
+
+#define FC_IPC_HANDLE_BYTES 64
+
+/* ---------------------------------------------------------------- heap ----
+ * The symmetric heap: one device allocation per rank whose first
+ * firecaffe_heap_reserved_bytes() bytes hold the library's synchronisation
+ * flags.  Collective buffers are carved from the rest at identical offsets on
+ * every rank (the caller does the carving).
+ */
+
+/* Bytes reserved at the start of a heap of `heap_bytes` (flag area; depends only
+ * on heap_bytes).  User buffers must start at or after this offset. */
+int64_t firecaffe_heap_reserved_bytes(int64_t heap_bytes);
+
+/* cudaMalloc `bytes` on the current device and zero them.  *heap receives the
+ * device pointer (256-byte aligned).  Free with firecaffe_heap_free. */
+fc_status firecaffe_heap_alloc(int64_t bytes, void** heap);
+fc_status firecaffe_heap_free(void* heap);
+
+/* Export a heap for other processes of the node: writes FC_IPC_HANDLE_BYTES
+ * opaque bytes (a cudaIpcMemHandle_t) to handle_out.  `heap` must be a pointer
+ * returned by firecaffe_heap_alloc. */
+fc_status firecaffe_heap_export(void* heap, uint8_t* handle_out);
+
+/* --------------------------------------------------------------- world ----
+ * firecaffe_world_create: the real world, one process per GPU.
+ *   rank, world_size : this process's rank in [0, world_size), world_size in 1..8
+ *   cuda_device      : the device this rank uses (must be current on the calling thread)
+ *   local_heap       : this rank's heap from firecaffe_heap_alloc (heap_bytes bytes)
+ *   handles          : world_size * FC_IPC_HANDLE_BYTES bytes, rank-ordered exports of every
+ *                      rank's heap (entry `rank` is ignored); exchanged by the caller
+ *                      (e.g. torch.distributed all_gather_object)
+ *   timeout_ns       : bound on every device-side wait (0 -> 30 s)
+ * Opens every peer heap with CUDA IPC (peer access over NVLink).  Collective:
+ * every rank must call it.  The flag area of local_heap must still be zero
+ * (fresh firecaffe_heap_alloc) — flags are never reset afterwards.
+ *
+ * firecaffe_world_create_virtual: p ranks emulated on ONE GPU, for testing the
+ * multi-rank schedules on a single device.  `heap` holds world_size consecutive
+ * rank heaps of heap_bytes_per_rank bytes each (allocate with firecaffe_heap_alloc
+ * (world_size * heap_bytes_per_rank)).  Collective calls on a virtual world take
+ * rank 0's buffer pointers; rank r's are at + r * heap_bytes_per_rank, for grad, w
+ * AND mom.  One cooperative kernel runs all ranks (rank = blockIdx.y).
+ */
+fc_status firecaffe_world_create(int rank, int world_size, int cuda_device, void* local_heap,
+                                 const uint8_t* handles, int64_t heap_bytes, uint64_t timeout_ns,
+                                 fc_world** out);
+fc_status firecaffe_world_create_virtual(int world_size, int cuda_device, void* heap,
+                                         int64_t heap_bytes_per_rank, uint64_t timeout_ns,
+                                         fc_world** out);
+fc_status firecaffe_world_destroy(fc_world* world);
+
+/* Select the executor.  arity k (2..world_size) is the tree's branching factor
+ * ("the base of log(p) depends on the branching factor"); arity > 2 and
+ * FC_SCHED_FOREST needs arity 2 and a power-of-two world size, FC_SCHED_SINGLE_ROOT
+ * needs arity 2; other combinations give FC_ERR_UNSUPPORTED and leave the
+ * configuration unchanged.  The default chosen at world creation (the fastest
+ * measured executor) is reported by firecaffe_world_get_config. */
+fc_status firecaffe_world_config(fc_world* world, int arity, fc_sched sched, fc_bcast bcast);
+fc_status firecaffe_world_get_config(const fc_world* world, int* arity, fc_sched* sched,
+                                     fc_bcast* bcast);
+
+/* Synchronise the device and return the sticky device status (FC_OK, or
+ * FC_ERR_TIMEOUT if any wait of any earlier call timed out). */
+fc_status firecaffe_world_poll(fc_world* world);
+
+/* The element range [*begin, *end) of the n-element vector whose momentum this
+ * rank updates in firecaffe_tree_allreduce_sgd (its subtree-root slice): the
+ * whole vector for world_size 1, rank 0's [0,n) for FC_SCHED_SINGLE_ROOT, an
+ * owner slice for FOREST/FLAT.  Host-only; no GPU needed. */
+fc_status firecaffe_owned_range(const fc_world* world, int rank, int64_t n, int64_t* begin,
+                                int64_t* end);
+/* Same, from (world_size, schedule) alone (host-only helper for tests/tools). */
+fc_status firecaffe_plan_owned_range(int world_size, fc_sched sched, int rank, int64_t n,
+                                     int64_t* begin, int64_t* end);
+
+/* ----------------------------------------------------------------- ops ----
+ * firecaffe_sgd_step — one SGD step with momentum and weight decay on one GPU
+ * (mu, wd P:358/P:363; Caffe convention, R6).  For i < n:
+ *     g  = fl(grad[i] * fl(1/batch))      grad is the gradient SUM over `batch` images
+ *     d  = fma(wd, w[i], g)
+ *     v' = fma(mu, mom[i], fl(lr * d))
+ *     w' = fl(w[i] - v')
+ * w and mom are updated in place; grad is read-only.  lr is used as given (already
+ * scaled for the batch, see firecaffe_scale_lr).  n == 0 is a no-op.
+ * Errors: FC_ERR_INVALID_ARG for null/unaligned pointers with n > 0, n < 0,
+ * lr <= 0, mu outside [0,1), wd < 0, batch < 1, overlapping buffers.
+ */
+fc_status firecaffe_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr,
+                             float mu, float wd, int64_t batch, void* stream);
+
+/* firecaffe_tree_allreduce — in place: on return (stream order) every rank's
+ * grad[0..n) holds the reduction-tree sum of all ranks' grad.
+ * Association (R1): k-nomial tree rooted at rank 0 in absolute rank
+ * space; at step s = k^l node r (r mod k*s == 0) adds r + j*s, j = 1..k-1 ascending.
+ * k=2: p=4 -> (g0+g1)+(g2+g3);  p=8 -> ((g0+g1)+(g2+g3))+((g4+g5)+(g6+g7)).
+ * Every schedule produces these bits.  world_size 1: no-op. */
+fc_status firecaffe_tree_allreduce(float* grad, int64_t n, fc_world* world, void* stream);
+
+/* firecaffe_tree_allreduce_sgd — the fused hot path: tree-reduce grad, apply the
+ * firecaffe_sgd_step update to the reduced gradient inside the final tree level
+ * (the sum never round-trips HBM), and broadcast the updated weights.  On return
+ * every rank's w[0..n) holds identical updated weights, bitwise equal to
+ * firecaffe_tree_allreduce followed by firecaffe_sgd_step.  mom is updated only on
+ * this rank's firecaffe_owned_range (the optimizer state is sharded across the
+ * subtree roots, R18); grad's contents are unspecified afterwards.
+ * world_size 1: identical to firecaffe_sgd_step.  Argument errors as sgd_step. */
+fc_status firecaffe_tree_allreduce_sgd(float* w, float* grad, float* mom, int64_t n, float lr,
+                                       float mu, float wd, int64_t batch, fc_world* world,
+                                       void* stream);
+
+/* firecaffe_ps_allreduce — the paper's synchronous parameter server (P:246-250,
+ * P:267-269) as the measured comparison: rank 0 (also a worker, R3)
+ * pulls every rank's grad, sums them sequentially in ascending rank order
+ * ((g0+g1)+g2)+..., and sends the sum to every rank: in place, every rank's grad
+ * holds it on return.  Equal bitwise to firecaffe_tree_allreduce with arity p. */
+fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* world, void* stream);
+
+/* Linear learning-rate scaling with the batch size:
+ * returns fl(base_lr * batch / base_batch) computed in double, e.g. (0.01, 256, 1024) -> 0.04.
+ * Returns 0 for base_batch < 1 or batch < 1. */
+float firecaffe_scale_lr(float base_lr, int64_t base_batch, int64_t batch);
+
+const char* firecaffe_status_str(fc_status s);
+
+/* Tuning knob for firecaffe_sgd_step: float4s in flight per thread per operand
+ * (1, 2, 4 or 8; default 4).  Process-wide; value-neutral. */
+void firecaffe_tune_sgd_unroll(int unroll);
+
+/* Library build identifier ("firecaffe-b200 <version> sm_100a"). */
+const char* firecaffe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FIRECAFFE_H */

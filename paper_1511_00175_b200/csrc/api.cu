@@ -1,0 +1,394 @@
+// The C ABI of libfirecaffe (include/firecaffe.h): argument validation,
+// the symmetric heap, world creation (CUDA IPC peer mapping over NVLink or a
+// virtual world on one GPU), executor selection and kernel launch.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+
+#include "fc_internal.h"
+#include "fc_launch.h"
+
+#define FC_VERSION_STR "firecaffe-b200 0.1.0 sm_100a"
+
+struct fc_world {
+    int rank;  // -1 for a virtual world
+    int p;
+    int device;
+    int virt;
+    char* heap_local;      // this rank's heap (virtual: rank 0's)
+    int64_t heap_bytes;    // per rank
+    char* peer[FC_MAX_RANKS];
+    bool opened[FC_MAX_RANKS];
+    uint32_t epoch;
+    uint64_t timeout_ns;
+    int* d_status;
+    int arity;
+    fc_sched sched;
+    fc_bcast bcast;
+    FcFlagLayout layout;
+};
+
+namespace fc {
+const DevInfo& dev_info() {
+    static DevInfo cache[64];
+    static bool have[64];
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= 64) d = 0;
+    if (!have[d]) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        cache[d].device = d;
+        cache[d].sms = sms > 0 ? sms : 1;
+        have[d] = true;
+    }
+    return cache[d];
+}
+}  // namespace fc
+
+using namespace fc;
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static bool overlap(const void* a, const void* b, int64_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + (uintptr_t)bytes && y < x + (uintptr_t)bytes;
+}
+
+static fc_status check_hyper(float lr, float mu, float wd, int64_t batch) {
+    if (!(lr > 0.0f) || !std::isfinite(lr)) return FC_ERR_INVALID_ARG;
+    if (!(mu >= 0.0f && mu < 1.0f)) return FC_ERR_INVALID_ARG;
+    if (!(wd >= 0.0f) || !std::isfinite(wd)) return FC_ERR_INVALID_ARG;
+    if (batch < 1) return FC_ERR_INVALID_ARG;
+    return FC_OK;
+}
+
+static fc_status check_vec(const void* p, int64_t n) {
+    if (n > 0 && (!p || !aligned16(p))) return FC_ERR_INVALID_ARG;
+    return FC_OK;
+}
+
+// float inv_b = 1 / (float)batch, one fp32 rounding (R7)
+static float inv_batch(int64_t batch) {
+    const volatile float one = 1.0f;
+    const volatile float b = (float)batch;
+    return one / b;
+}
+
+extern "C" {
+
+const char* firecaffe_version(void) { return FC_VERSION_STR; }
+
+const char* firecaffe_status_str(fc_status s) {
+    switch (s) {
+        case FC_OK: return "ok";
+        case FC_ERR_INVALID_ARG: return "invalid argument";
+        case FC_ERR_NOT_SYMMETRIC: return "buffer not in the symmetric heap";
+        case FC_ERR_MISMATCH: return "world/device mismatch";
+        case FC_ERR_TIMEOUT: return "timeout waiting for a peer";
+        case FC_ERR_CUDA: return "CUDA error";
+        case FC_ERR_UNSUPPORTED: return "unsupported schedule for this world";
+    }
+    return "unknown status";
+}
+
+float firecaffe_scale_lr(float base_lr, int64_t base_batch, int64_t batch) {
+    if (base_batch < 1 || batch < 1) return 0.0f;
+    return (float)((double)base_lr * (double)batch / (double)base_batch);
+}
+
+int64_t firecaffe_heap_reserved_bytes(int64_t heap_bytes) {
+    if (heap_bytes < 0) return -1;
+    return fc_flag_layout(heap_bytes).total_bytes;
+}
+
+fc_status firecaffe_heap_alloc(int64_t bytes, void** heap) {
+    if (!heap || bytes <= 0) return FC_ERR_INVALID_ARG;
+    *heap = nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, (size_t)bytes) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMemset(p, 0, (size_t)bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaFree(p);
+        return FC_ERR_CUDA;
+    }
+    *heap = p;
+    return FC_OK;
+}
+
+fc_status firecaffe_heap_free(void* heap) {
+    if (!heap) return FC_OK;
+    return cudaFree(heap) == cudaSuccess ? FC_OK : FC_ERR_CUDA;
+}
+
+fc_status firecaffe_heap_export(void* heap, uint8_t* handle_out) {
+    if (!heap || !handle_out) return FC_ERR_INVALID_ARG;
+    static_assert(sizeof(cudaIpcMemHandle_t) == FC_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, heap) != cudaSuccess) return FC_ERR_CUDA;
+    memcpy(handle_out, &h, sizeof(h));
+    return FC_OK;
+}
+
+static void default_config(fc_world* w) {
+    w->arity = 2;
+    w->sched = is_pow2(w->p) ? FC_SCHED_FOREST : FC_SCHED_FLAT;
+    w->bcast = FC_BCAST_DIRECT;
+}
+
+static fc_status world_common(fc_world* w, int world_size, int dev, int64_t heap_bytes,
+                              uint64_t timeout_ns) {
+    w->p = world_size;
+    w->device = dev;
+    w->heap_bytes = heap_bytes;
+    w->epoch = 0;
+    w->timeout_ns = timeout_ns ? timeout_ns : 30ull * 1000000000ull;
+    w->layout = fc_flag_layout(heap_bytes);
+    if (w->layout.total_bytes >= heap_bytes) return FC_ERR_INVALID_ARG;
+    if (cudaMalloc(&w->d_status, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMemset(w->d_status, 0, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
+    default_config(w);
+    return FC_OK;
+}
+
+fc_status firecaffe_world_create(int rank, int world_size, int cuda_device, void* local_heap,
+                                 const uint8_t* handles, int64_t heap_bytes, uint64_t timeout_ns,
+                                 fc_world** out) {
+    if (!out) return FC_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (world_size < 1 || world_size > FC_MAX_RANKS || rank < 0 || rank >= world_size)
+        return FC_ERR_INVALID_ARG;
+    if (!local_heap || heap_bytes <= 0 || (world_size > 1 && !handles)) return FC_ERR_INVALID_ARG;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
+    if (cur != cuda_device) return FC_ERR_MISMATCH;
+    fc_world* w = new fc_world();
+    memset(w, 0, sizeof(*w));
+    w->rank = rank;
+    w->virt = 0;
+    w->heap_local = (char*)local_heap;
+    fc_status st = world_common(w, world_size, cuda_device, heap_bytes, timeout_ns);
+    if (st != FC_OK) {
+        firecaffe_world_destroy(w);
+        return st;
+    }
+    for (int q = 0; q < world_size; ++q) {
+        if (q == rank) {
+            w->peer[q] = (char*)local_heap;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handles + (size_t)q * FC_IPC_HANDLE_BYTES, sizeof(h));
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            firecaffe_world_destroy(w);
+            return FC_ERR_CUDA;
+        }
+        w->peer[q] = (char*)p;
+        w->opened[q] = true;
+    }
+    *out = w;
+    return FC_OK;
+}
+
+fc_status firecaffe_world_create_virtual(int world_size, int cuda_device, void* heap,
+                                         int64_t heap_bytes_per_rank, uint64_t timeout_ns,
+                                         fc_world** out) {
+    if (!out) return FC_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (world_size < 1 || world_size > FC_MAX_RANKS || !heap || heap_bytes_per_rank <= 0 ||
+        (heap_bytes_per_rank & 255) != 0)
+        return FC_ERR_INVALID_ARG;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
+    if (cur != cuda_device) return FC_ERR_MISMATCH;
+    fc_world* w = new fc_world();
+    memset(w, 0, sizeof(*w));
+    w->rank = -1;
+    w->virt = 1;
+    w->heap_local = (char*)heap;
+    fc_status st = world_common(w, world_size, cuda_device, heap_bytes_per_rank, timeout_ns);
+    if (st != FC_OK) {
+        firecaffe_world_destroy(w);
+        return st;
+    }
+    for (int q = 0; q < world_size; ++q) w->peer[q] = (char*)heap + (int64_t)q * heap_bytes_per_rank;
+    *out = w;
+    return FC_OK;
+}
+
+fc_status firecaffe_world_destroy(fc_world* w) {
+    if (!w) return FC_OK;
+    fc_status st = FC_OK;
+    for (int q = 0; q < FC_MAX_RANKS; ++q)
+        if (w->opened[q] && cudaIpcCloseMemHandle(w->peer[q]) != cudaSuccess) st = FC_ERR_CUDA;
+    if (w->d_status) cudaFree(w->d_status);
+    delete w;
+    return st;
+}
+
+fc_status firecaffe_world_config(fc_world* w, int arity, fc_sched sched, fc_bcast bcast) {
+    if (!w) return FC_ERR_INVALID_ARG;
+    if (arity < 2 || (bcast != FC_BCAST_TREE && bcast != FC_BCAST_DIRECT)) return FC_ERR_INVALID_ARG;
+    if (sched != FC_SCHED_FOREST && sched != FC_SCHED_SINGLE_ROOT && sched != FC_SCHED_FLAT)
+        return FC_ERR_INVALID_ARG;
+    if (sched == FC_SCHED_FOREST && (arity != 2 || !is_pow2(w->p))) return FC_ERR_UNSUPPORTED;
+    if (sched == FC_SCHED_SINGLE_ROOT && arity != 2) return FC_ERR_UNSUPPORTED;
+    w->arity = arity;
+    w->sched = sched;
+    w->bcast = bcast;
+    return FC_OK;
+}
+
+fc_status firecaffe_world_get_config(const fc_world* w, int* arity, fc_sched* sched,
+                                     fc_bcast* bcast) {
+    if (!w) return FC_ERR_INVALID_ARG;
+    if (arity) *arity = w->arity;
+    if (sched) *sched = w->sched;
+    if (bcast) *bcast = w->bcast;
+    return FC_OK;
+}
+
+fc_status firecaffe_world_poll(fc_world* w) {
+    if (!w) return FC_ERR_INVALID_ARG;
+    if (cudaDeviceSynchronize() != cudaSuccess) return FC_ERR_CUDA;
+    int s = 0;
+    if (cudaMemcpy(&s, w->d_status, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return FC_ERR_CUDA;
+    return (fc_status)s;
+}
+
+fc_status firecaffe_plan_owned_range(int world_size, fc_sched sched, int rank, int64_t n,
+                                     int64_t* begin, int64_t* end) {
+    if (!begin || !end || world_size < 1 || world_size > FC_MAX_RANKS || rank < 0 ||
+        rank >= world_size || n < 0)
+        return FC_ERR_INVALID_ARG;
+    if (world_size == 1) {
+        *begin = 0;
+        *end = n;
+        return FC_OK;
+    }
+    const int64_t nch = (n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    int64_t c0, c1;
+    owned_chunks(rank, world_size, nch, sched == FC_SCHED_SINGLE_ROOT, &c0, &c1);
+    int64_t b = c0 * FC_CHUNK_FLOATS, e = c1 * FC_CHUNK_FLOATS;
+    if (b > n) b = n;
+    if (e > n) e = n;
+    if (e < b) e = b;
+    *begin = b;
+    *end = e;
+    return FC_OK;
+}
+
+fc_status firecaffe_owned_range(const fc_world* w, int rank, int64_t n, int64_t* begin,
+                                int64_t* end) {
+    if (!w) return FC_ERR_INVALID_ARG;
+    return firecaffe_plan_owned_range(w->p, w->sched, rank, n, begin, end);
+}
+
+fc_status firecaffe_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr,
+                             float mu, float wd, int64_t batch, void* stream) {
+    if (n < 0) return FC_ERR_INVALID_ARG;
+    fc_status st = check_hyper(lr, mu, wd, batch);
+    if (st != FC_OK) return st;
+    if (n == 0) return FC_OK;
+    if (check_vec(w, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    const int64_t bytes = n * 4;
+    if (overlap(w, grad, bytes) || overlap(w, mom, bytes) || overlap(grad, mom, bytes))
+        return FC_ERR_INVALID_ARG;
+    cudaError_t e = launch_sgd_step(w, grad, mom, n, lr, mu, wd, inv_batch(batch),
+                                    (cudaStream_t)stream);
+    return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
+}
+
+// Offset of a symmetric buffer inside this rank's heap, or -1.
+static int64_t heap_offset(const fc_world* w, const void* p, int64_t n) {
+    const char* c = (const char*)p;
+    const int64_t off = c - w->heap_local;
+    if (c < w->heap_local || off < w->layout.total_bytes) return -1;
+    if (off + n * 4 > w->heap_bytes) return -1;
+    return off;
+}
+
+static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* mom, int64_t n,
+                            float lr, float mu, float wd, int64_t batch, void* stream) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
+    if (cur != w->device) return FC_ERR_MISMATCH;
+    FcColl c;
+    memset(&c, 0, sizeof(c));
+    c.off_grad = heap_offset(w, grad, n);
+    if (c.off_grad < 0) return FC_ERR_NOT_SYMMETRIC;
+    c.off_w = 0;
+    c.off_mom = -1;
+    if (op == FC_OP_ALLREDUCE_SGD) {
+        c.off_w = heap_offset(w, wt, n);
+        if (c.off_w < 0) return FC_ERR_NOT_SYMMETRIC;
+        if (w->virt) {
+            c.off_mom = heap_offset(w, mom, n);
+            if (c.off_mom < 0) return FC_ERR_NOT_SYMMETRIC;
+        }
+        c.mom_local = mom;
+        c.lr = lr;
+        c.mu = mu;
+        c.wd = wd;
+        c.inv_b = inv_batch(batch);
+    }
+    for (int q = 0; q < w->p; ++q) c.peers.heap[q] = w->peer[q];
+    c.rank = w->virt ? -1 : w->rank;
+    c.p = w->p;
+    c.epoch = ++w->epoch;
+    c.op = op;
+    c.timeout_ns = w->timeout_ns;
+    c.status = w->d_status;
+    c.n = n;
+    c.bcast = w->bcast;
+    c.bar_words = w->layout.bar_words;
+    c.red_words = w->layout.red_words;
+    c.max_chunks = w->layout.max_chunks;
+    const int sched = op == FC_OP_PS ? FC_SCHED_FLAT : w->sched;
+    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op == FC_OP_PS);
+    if (grid < 1) return FC_ERR_UNSUPPORTED;
+    cudaError_t e = launch_collective(c, sched, w->arity, w->virt != 0, grid, (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        --w->epoch;
+        return FC_ERR_CUDA;
+    }
+    return FC_OK;
+}
+
+fc_status firecaffe_tree_allreduce(float* grad, int64_t n, fc_world* w, void* stream) {
+    if (!w || n < 0) return FC_ERR_INVALID_ARG;
+    if (n == 0 || w->p == 1) return FC_OK;
+    if (check_vec(grad, n)) return FC_ERR_INVALID_ARG;
+    return collective(w, FC_OP_ALLREDUCE, nullptr, grad, nullptr, n, 0, 0, 0, 1, stream);
+}
+
+fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* w, void* stream) {
+    if (!w || n < 0) return FC_ERR_INVALID_ARG;
+    if (n == 0 || w->p == 1) return FC_OK;
+    if (check_vec(grad, n)) return FC_ERR_INVALID_ARG;
+    return collective(w, FC_OP_PS, nullptr, grad, nullptr, n, 0, 0, 0, 1, stream);
+}
+
+fc_status firecaffe_tree_allreduce_sgd(float* wt, float* grad, float* mom, int64_t n, float lr,
+                                       float mu, float wd, int64_t batch, fc_world* w,
+                                       void* stream) {
+    if (!w || n < 0) return FC_ERR_INVALID_ARG;
+    fc_status st = check_hyper(lr, mu, wd, batch);
+    if (st != FC_OK) return st;
+    if (n == 0) return FC_OK;
+    if (check_vec(wt, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    const int64_t bytes = n * 4;
+    if (overlap(wt, grad, bytes) || overlap(wt, mom, bytes) || overlap(grad, mom, bytes))
+        return FC_ERR_INVALID_ARG;
+    if (w->p == 1) return firecaffe_sgd_step(wt, grad, mom, n, lr, mu, wd, batch, stream);
+    return collective(w, FC_OP_ALLREDUCE_SGD, wt, grad, mom, n, lr, mu, wd, batch, stream);
+}
+
+void firecaffe_tune_sgd_unroll(int u) { set_sgd_unroll(u); }
+
+}  // extern "C"

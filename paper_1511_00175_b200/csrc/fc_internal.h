@@ -1,0 +1,59 @@
+// Internal host/device structures of libfirecaffe (not part of the C ABI).
+#pragma once
+#include <stdint.h>
+
+#include "../../include/firecaffe.h"
+
+#define FC_MAX_RANKS 8
+#define FC_MAX_CTAS 1024
+#define FC_MAX_LEVELS 3          // log2(FC_MAX_RANKS)
+#define FC_CHUNK_FLOATS 4096     // flag granularity of the level-structured schedules (16 KB)
+#define FC_BAR_SLOTS 2           // 0 = entry barrier, 1 = exit barrier
+
+// Layout of the flag area at the start of every rank's heap (uint32 words):
+//   bar[FC_BAR_SLOTS][FC_MAX_CTAS][FC_MAX_RANKS]   per-CTA all-to-all barriers
+//   red[FC_MAX_LEVELS][max_chunks]                 "partial of chunk c for level l+1 ready"
+//   av[max_chunks]                                 "broadcast value of chunk c has arrived"
+// All flags hold the epoch of the call that last wrote them (monotonic, never reset).
+struct FcFlagLayout {
+    int64_t max_chunks;
+    int64_t bar_words;   // offset of red[] in words
+    int64_t red_words;   // offset of av[] in words
+    int64_t total_bytes; // reserved prefix, rounded to 64 KB
+};
+
+static inline FcFlagLayout fc_flag_layout(int64_t heap_bytes) {
+    FcFlagLayout L;
+    L.max_chunks = heap_bytes / (4 * (int64_t)FC_CHUNK_FLOATS) + 1;
+    L.bar_words = (int64_t)FC_BAR_SLOTS * FC_MAX_CTAS * FC_MAX_RANKS;
+    L.red_words = L.bar_words + (int64_t)FC_MAX_LEVELS * L.max_chunks;
+    int64_t words = L.red_words + L.max_chunks;
+    int64_t bytes = words * 4;
+    L.total_bytes = (bytes + 65535) / 65536 * 65536;
+    return L;
+}
+
+// Everything a collective kernel needs to find every rank's buffers.
+struct FcPeers {
+    char* heap[FC_MAX_RANKS];  // each rank's heap base, as mapped in this process
+};
+
+struct FcColl {
+    FcPeers peers;
+    int rank;          // >= 0: this process's rank; -1: virtual world, rank = blockIdx.y
+    int p;             // world size
+    uint32_t epoch;    // call counter (same on every rank)
+    int op;            // FcOp
+    uint64_t timeout_ns;
+    int* status;       // sticky device status (FC_OK until a timeout)
+    int64_t n;         // floats
+    int64_t off_grad;  // byte offsets of the symmetric buffers inside each heap
+    int64_t off_w;
+    int64_t off_mom;   // >= 0: mom is symmetric in the heap; < 0: use mom_local
+    float* mom_local;
+    float lr, mu, wd, inv_b;
+    int bcast;         // fc_bcast
+    int64_t bar_words, red_words, max_chunks;
+};
+
+enum FcOp { FC_OP_ALLREDUCE = 0, FC_OP_ALLREDUCE_SGD = 1, FC_OP_PS = 2 };

@@ -1,0 +1,49 @@
+// Host-side launch interface between the C ABI (api.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fc_internal.h"
+
+namespace fc {
+
+struct DevInfo {
+    int device;
+    int sms;
+};
+const DevInfo& dev_info();  // current device's SM count (cached per device)
+
+cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
+                            float wd, float inv_b, cudaStream_t st);
+void set_sgd_unroll(int u);
+
+// Collective launch: `virt` -> one cooperative grid of (grid_x, p) CTAs that emulates all ranks.
+cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
+                              cudaStream_t st);
+// Max CTAs per rank that can be co-resident for this schedule (virt: divided by p).
+int collective_grid(int sched, int arity, int p, bool virt, bool ps);
+
+// Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
+__host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }
+__host__ __device__ inline void owned_chunks(int rank, int p, int64_t n_chunks, bool single_root,
+                                             int64_t* c0, int64_t* c1) {
+    if (single_root) {
+        *c0 = 0;
+        *c1 = rank == 0 ? n_chunks : 0;
+        return;
+    }
+    if (is_pow2(p)) {  // recursive halving: level l keeps the half selected by bit l of rank
+        int64_t lo = 0, hi = n_chunks;
+        for (int l = 0; (1 << l) < p; ++l) {
+            const int64_t mid = lo + (hi - lo + 1) / 2;
+            if ((rank >> l) & 1) lo = mid; else hi = mid;
+        }
+        *c0 = lo;
+        *c1 = hi;
+    } else {
+        *c0 = (int64_t)rank * n_chunks / p;
+        *c1 = (int64_t)(rank + 1) * n_chunks / p;
+    }
+}
+
+}  // namespace fc

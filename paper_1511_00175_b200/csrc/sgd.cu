@@ -1,0 +1,86 @@
+// firecaffe_sgd_step kernel: the 1-GPU fused SGD update.
+//
+// HBM-bound streaming kernel: per parameter it reads grad, w, mom and writes
+// w, mom (20 algorithmic bytes).  128-bit accesses, U independent float4 per
+// thread per operand in flight (all loads issued before any math), grid sized
+// to the SM count x resident CTAs so every SM streams.
+#include <cuda_runtime.h>
+
+#include "fc_device.cuh"
+#include "fc_launch.h"
+
+namespace fc {
+
+template <int U>
+__global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
+                                                       const float4* __restrict__ g4,
+                                                       float4* __restrict__ v4, int64_t n4,
+                                                       float* __restrict__ wt,
+                                                       const float* __restrict__ gt,
+                                                       float* __restrict__ vt, int tail, float lr,
+                                                       float mu, float wd, float inv_b) {
+    const int64_t T = blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    for (int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x; base < n4; base += stride) {
+        float4 g[U], w[U], v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = base + j * T;
+            if (i < n4) {
+                g[j] = ld_stream(g4 + i);
+                w[j] = ld_rw(w4 + i);
+                v[j] = ld_rw(v4 + i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = base + j * T;
+            if (i < n4) {
+                sgd4(g[j], w[j], v[j], lr, mu, wd, inv_b);
+                st_na(w4 + i, w[j]);
+                st_na(v4 + i, v[j]);
+            }
+        }
+    }
+    // the n % 4 trailing elements
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < tail) {
+        const int t = threadIdx.x;
+        float w = wt[t], v = vt[t];
+        sgd1(gt[t], w, v, lr, mu, wd, inv_b);
+        wt[t] = w;
+        vt[t] = v;
+    }
+}
+
+static int g_sgd_unroll = 4;
+
+cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
+                            float wd, float inv_b, cudaStream_t st) {
+    const int64_t n4 = n / 4;
+    const int tail = (int)(n - n4 * 4);
+    const int T = 256;
+    const DevInfo& di = dev_info();
+    auto run = [&](auto kern, int U) -> cudaError_t {
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, 0);
+        if (e != cudaSuccess) return e;
+        int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
+        int64_t cap = (int64_t)di.sms * (occ > 0 ? occ : 1);
+        int64_t grid = want < cap ? want : cap;
+        if (grid < 1) grid = 1;
+        kern<<<(unsigned)grid, T, 0, st>>>((float4*)w, (const float4*)grad, (float4*)mom, n4,
+                                           w + n4 * 4, grad + n4 * 4, mom + n4 * 4, tail, lr, mu,
+                                           wd, inv_b);
+        return cudaGetLastError();
+    };
+    switch (g_sgd_unroll) {
+        case 1: return run(sgd_step_kernel<1>, 1);
+        case 2: return run(sgd_step_kernel<2>, 2);
+        case 8: return run(sgd_step_kernel<8>, 8);
+        default: return run(sgd_step_kernel<4>, 4);
+    }
+}
+
+void set_sgd_unroll(int u) { g_sgd_unroll = u; }
+
+}  // namespace fc

@@ -1,0 +1,497 @@
+// Collective kernels of libfirecaffe: the reduction tree over NVLink peer
+// memory, one persistent cooperative kernel per call.
+//
+// Every rank's heap is mapped into every process (CUDA IPC), so a kernel reads
+// a peer GPU's gradient slice with ordinary 128-bit loads and writes a peer's
+// weights with ordinary 128-bit stores; both cross NVLink / NVSwitch.  Order
+// between GPUs comes from epoch-stamped flags in the heaps' reserved prefix
+// (st.release.sys / ld.acquire.sys).  Producers PUSH flags to the consumer's
+// heap so that every spin is on local memory.
+//
+// Schedules (include/firecaffe.h fc_sched) — all produce the same bits, the
+// k-nomial association of DESIGN.md R1:
+//   FLAT        each rank pulls its owner slice from all p ranks, evaluates
+//               the whole tree in registers, applies SGD, pushes w' to all.
+//   FOREST      recursive halving: at level l rank r pulls |W|/2^(l+1) from
+//               r^2^l (the binomial tree of slice s is rooted at its owner);
+//               SGD fused into the last level; tree or direct broadcast.
+//   SINGLE_ROOT the paper's binomial tree rooted at rank 0 (Fig. P:312-315);
+//               the root applies SGD to all of W, then broadcast.
+//   PS          (op FC_OP_PS) rank 0 pulls everything, sequential sum, pushes.
+// Static work mapping: chunk cc (FC_CHUNK_FLOATS floats) is always processed
+// by CTA cc % gridDim.x, element k of a chunk always by the same thread, so a
+// rank's own partial sums need no flags between levels (program order).
+#include <cuda_runtime.h>
+
+#include "fc_device.cuh"
+#include "fc_launch.h"
+
+namespace fc {
+
+constexpr int TREE_T = 256;                       // threads per CTA
+constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
+constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
+static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
+
+// ------------------------------------------------------------ addressing ---
+__device__ __forceinline__ int my_rank(const FcColl& c) {
+    return c.rank >= 0 ? c.rank : (int)blockIdx.y;
+}
+__device__ __forceinline__ uint32_t* flag_base(const FcColl& c, int q) {
+    return reinterpret_cast<uint32_t*>(c.peers.heap[q]);
+}
+__device__ __forceinline__ uint32_t* bar_flag(const FcColl& c, int owner, int slot, int cta,
+                                              int src) {
+    return flag_base(c, owner) + ((int64_t)(slot * FC_MAX_CTAS + cta) * FC_MAX_RANKS + src);
+}
+__device__ __forceinline__ uint32_t* red_flag(const FcColl& c, int owner, int l, int64_t cc) {
+    return flag_base(c, owner) + c.bar_words + (int64_t)l * c.max_chunks + cc;
+}
+__device__ __forceinline__ uint32_t* av_flag(const FcColl& c, int owner, int64_t cc) {
+    return flag_base(c, owner) + c.red_words + cc;
+}
+__device__ __forceinline__ float* grad_of(const FcColl& c, int q) {
+    return reinterpret_cast<float*>(c.peers.heap[q] + c.off_grad);
+}
+__device__ __forceinline__ float* w_of(const FcColl& c, int q) {
+    return reinterpret_cast<float*>(c.peers.heap[q] + c.off_w);
+}
+__device__ __forceinline__ float* mom_of(const FcColl& c, int q) {
+    return c.off_mom >= 0 ? reinterpret_cast<float*>(c.peers.heap[q] + c.off_mom) : c.mom_local;
+}
+
+// ------------------------------------------------------------ sync ---------
+// All-to-all barrier among the CTAs with this blockIdx.x on every rank
+// (slot 0 = entry, 1 = exit).  Thread q < p pushes "rank arrived" into rank q's
+// heap, then spins on rank q's stamp in the local heap.  The fence orders the
+// CTA's earlier writes (peer stores included; the caller's __syncthreads
+// orders the other threads' writes before it) ahead of the flag.
+__device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
+    __syncthreads();
+    const int t = threadIdx.x;
+    bool good = true;
+    if (t < c.p && t != rank) {
+        fence_sys();
+        st_release_sys(bar_flag(c, t, slot, blockIdx.x, rank), c.epoch);
+        good = wait_flag(bar_flag(c, rank, slot, blockIdx.x, t), c.epoch, c.timeout_ns, c.status);
+    }
+    return __syncthreads_and(good) != 0;
+}
+
+// One thread waits for a flag; the CTA learns the outcome.
+__device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
+    bool good = true;
+    if (threadIdx.x == 0) good = wait_flag(f, c.epoch, c.timeout_ns, c.status);
+    return __syncthreads_and(good) != 0;
+}
+
+// After the CTA finished writing a chunk: publish it with one flag.
+__device__ __forceinline__ void signal_one(const FcColl& c, uint32_t* f) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_sys();
+        st_release_sys(f, c.epoch);
+    }
+}
+
+__device__ __forceinline__ int64_t first_chunk(int64_t lo, int G, int b) {
+    const int64_t r = lo % G;
+    return lo + ((b - r) % G + G) % G;
+}
+
+// ------------------------------------------------------------ chunk ops ----
+// Level step on chunk cc: s = own partial + peer partial (R1: the
+// lower rank group's partial plus the upper group's; fp32 addition commutes
+// bitwise, so operand order is immaterial).  Not last: s -> own grad (in
+// place).  Last (subtree root): fused -> SGD on w, mom; unfused -> s -> grad.
+// `direct`: also push the result to every other rank.
+template <int P>
+__device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t cc, float* own,
+                                             const float* peer, bool last, bool fused,
+                                             bool direct) {
+    const int64_t e0 = cc * FC_CHUNK_FLOATS;
+    const int64_t e1 = min(e0 + (int64_t)FC_CHUNK_FLOATS, c.n);
+    const int nf4 = (int)((e1 - e0) >> 2);
+    const int rem = (int)((e1 - e0) & 3);
+    const int t = threadIdx.x;
+    float4* own4 = reinterpret_cast<float4*>(own + e0);
+    const float4* peer4 = reinterpret_cast<const float4*>(peer + e0);
+    float4 a[PER_T], b[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            a[j] = ld_cg(own4 + k);
+            b[j] = ld_cg(peer4 + k);
+        }
+    }
+    if (!last || !fused) {
+#pragma unroll
+        for (int j = 0; j < PER_T; ++j) {
+            const int k = j * TREE_T + t;
+            if (k < nf4) {
+                const float4 s = add4(a[j], b[j]);
+                st_na(own4 + k, s);
+                if (last && direct) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if (q != rank) st_na(reinterpret_cast<float4*>(grad_of(c, q) + e0) + k, s);
+                }
+            }
+        }
+        if (t < rem) {
+            const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+            const float s = __fadd_rn(ld_cg1(own + e), ld_cg1(peer + e));
+            st1(own + e, s);
+            if (last && direct)
+                for (int q = 0; q < P; ++q)
+                    if (q != rank) st1(grad_of(c, q) + e, s);
+        }
+        return;
+    }
+    // last level, fused SGD: the reduced gradient lives only in registers
+    float4* w4 = reinterpret_cast<float4*>(w_of(c, rank) + e0);
+    float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank) + e0);
+    float4 w[PER_T], v[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            w[j] = ld_rw(w4 + k);
+            v[j] = ld_rw(v4 + k);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            const float4 s = add4(a[j], b[j]);
+            sgd4(s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+            st_na(w4 + k, w[j]);
+            st_na(v4 + k, v[j]);
+            if (direct) {
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (q != rank) st_na(reinterpret_cast<float4*>(w_of(c, q) + e0) + k, w[j]);
+            }
+        }
+    }
+    if (t < rem) {
+        const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+        const float s = __fadd_rn(ld_cg1(own + e), ld_cg1(peer + e));
+        float* wp = w_of(c, rank) + e;
+        float* vp = mom_of(c, rank) + e;
+        float ww = *wp, vv = *vp;
+        sgd1(s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+        st1(wp, ww);
+        st1(vp, vv);
+        if (direct)
+            for (int q = 0; q < P; ++q)
+                if (q != rank) st1(w_of(c, q) + e, ww);
+    }
+}
+
+// Copy chunk cc of `src` (local) to up to 3 destinations (peers).
+__device__ __forceinline__ void copy_chunk(const FcColl& c, int64_t cc, const float* src,
+                                           float* const* dst, int ndst) {
+    const int64_t e0 = cc * FC_CHUNK_FLOATS;
+    const int64_t e1 = min(e0 + (int64_t)FC_CHUNK_FLOATS, c.n);
+    const int nf4 = (int)((e1 - e0) >> 2);
+    const int rem = (int)((e1 - e0) & 3);
+    const int t = threadIdx.x;
+    const float4* s4 = reinterpret_cast<const float4*>(src + e0);
+    float4 x[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) x[j] = ld_cg(s4 + k);
+    }
+    for (int d = 0; d < ndst; ++d) {
+        float4* d4 = reinterpret_cast<float4*>(dst[d] + e0);
+#pragma unroll
+        for (int j = 0; j < PER_T; ++j) {
+            const int k = j * TREE_T + t;
+            if (k < nf4) st_na(d4 + k, x[j]);
+        }
+    }
+    if (t < rem) {
+        const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+        const float v = ld_cg1(src + e);
+        for (int d = 0; d < ndst; ++d) st1(dst[d] + e, v);
+    }
+}
+
+// ------------------------------------------------------------ FLAT / PS ----
+// One communication level: the owner of slice [e0, e1) loads all P ranks'
+// values, evaluates the K-nomial tree in registers (K = P: the parameter
+// server's sequential order), then either applies SGD and pushes w' to every
+// rank (fused) or pushes the sum to every rank's grad.
+template <int P, int K, int U>
+__global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
+    const int rank = my_rank(c);
+    const bool ok = cta_barrier(c, rank, 0);
+    if (ok) {
+        const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+        int64_t c0, c1;
+        owned_chunks(rank, P, nch, c.op == FC_OP_PS, &c0, &c1);
+        const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+        const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+        const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
+        if (e1 > e0) {
+            const int64_t i0 = e0 / 4, i1 = e1 / 4;
+            const int64_t T = TREE_T;
+            const int64_t stride = (int64_t)gridDim.x * T * U;
+            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < i1;
+                 base += stride) {
+                float4 x[U][P];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int64_t i = base + j * T;
+                    if (i < i1) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            x[j][q] = ld_cg(reinterpret_cast<const float4*>(grad_of(c, q)) + i);
+                    }
+                }
+                if (fused) {
+                    float4 w[U], v[U];
+                    float4* w4 = reinterpret_cast<float4*>(w_of(c, rank));
+                    float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < i1) {
+                            w[j] = ld_rw(w4 + i);
+                            v[j] = ld_rw(v4 + i);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < i1) {
+                            const float4 S = tree_sum_regs<P, K>(x[j]);
+                            sgd4(S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                            st_na(v4 + i, v[j]);
+#pragma unroll
+                            for (int q = 0; q < P; ++q)
+                                st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < i1) {
+                            const float4 S = tree_sum_regs<P, K>(x[j]);
+#pragma unroll
+                            for (int q = 0; q < P; ++q)
+                                st_na(reinterpret_cast<float4*>(grad_of(c, q)) + i, S);
+                        }
+                    }
+                }
+            }
+            // trailing n % 4 elements of the last slice
+            const int rem = (int)(e1 - 4 * i1);
+            if (blockIdx.x == 0 && (int)threadIdx.x < rem) {
+                const int64_t e = 4 * i1 + threadIdx.x;
+                float xs[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) xs[q] = ld_cg1(grad_of(c, q) + e);
+                const float S = tree_sum_regs1<P, K>(xs);
+                if (fused) {
+                    float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
+                    sgd1(S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                    st1(mom_of(c, rank) + e, vv);
+                    for (int q = 0; q < P; ++q) st1(w_of(c, q) + e, ww);
+                } else {
+                    for (int q = 0; q < P; ++q) st1(grad_of(c, q) + e, S);
+                }
+            }
+        }
+    }
+    cta_barrier(c, rank, 1);
+}
+
+// ------------------------------------------------------------ FOREST -------
+template <int P>
+__global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
+    constexpr int M = (P >= 8) ? 3 : (P >= 4) ? 2 : (P >= 2) ? 1 : 0;
+    static_assert((1 << M) == P, "forest needs a power-of-two world");
+    const int rank = my_rank(c);
+    const int G = gridDim.x, b = blockIdx.x;
+    const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
+    const bool direct = c.bcast == FC_BCAST_DIRECT;
+    float* own = grad_of(c, rank);
+    bool ok = cta_barrier(c, rank, 0);
+
+    // ---- reduce: recursive halving, level l pairs rank with rank ^ 2^l
+    int64_t lo = 0, hi = nch;
+    for (int l = 0; l < M && ok; ++l) {
+        const int partner = rank ^ (1 << l);
+        const int64_t mid = lo + (hi - lo + 1) / 2;
+        if ((rank >> l) & 1) lo = mid; else hi = mid;
+        const bool last = (l == M - 1);
+        const int64_t mid_next = lo + (hi - lo + 1) / 2;
+        const bool keep_lower_next = ((rank >> (l + 1)) & 1) == 0;
+        const float* pg = grad_of(c, partner);
+        for (int64_t cc = first_chunk(lo, G, b); cc < hi; cc += G) {
+            if (l >= 1 && !wait_one(c, red_flag(c, rank, l - 1, cc))) { ok = false; break; }
+            reduce_chunk<P>(c, rank, cc, own, pg, last, fused, direct);
+            if (!last && ((cc < mid_next) != keep_lower_next))  // next-level consumer is the partner
+                signal_one(c, red_flag(c, rank ^ (1 << (l + 1)), l, cc));
+        }
+    }
+
+    // ---- broadcast back down the tree (recursive doubling), or direct
+    if (!direct) {
+        const int64_t o0 = lo, o1 = hi;  // owned slice
+        float* mine = fused ? w_of(c, rank) : own;
+        for (int j = 0; j < M && ok; ++j) {
+            const int l = M - 1 - j;
+            const int partner = rank ^ (1 << l);
+            int64_t rlo = 0, rhi = nch;  // region R_{l+1}(rank) held now
+            for (int i = 0; i <= l; ++i) {
+                const int64_t m2 = rlo + (rhi - rlo + 1) / 2;
+                if ((rank >> i) & 1) rlo = m2; else rhi = m2;
+            }
+            float* dst = fused ? w_of(c, partner) : grad_of(c, partner);
+            for (int64_t cc = first_chunk(rlo, G, b); cc < rhi; cc += G) {
+                const bool owned = cc >= o0 && cc < o1;
+                if (!owned && !wait_one(c, av_flag(c, rank, cc))) { ok = false; break; }
+                copy_chunk(c, cc, mine, &dst, 1);
+                signal_one(c, av_flag(c, partner, cc));
+            }
+        }
+        if (ok && M > 0) {  // chunks that arrive at the last level are not forwarded: wait for them
+            const int p0 = rank ^ 1;
+            const int64_t m0 = (nch + 1) / 2;
+            const int64_t rlo = (p0 & 1) ? m0 : 0, rhi = (p0 & 1) ? nch : m0;
+            for (int64_t cc = first_chunk(rlo, G, b); cc < rhi; cc += G)
+                if (!wait_one(c, av_flag(c, rank, cc))) break;
+        }
+    } else {
+        cta_barrier(c, rank, 1);
+    }
+}
+
+// ------------------------------------------------------------ SINGLE ROOT --
+// The paper's binomial tree rooted at rank 0: level l, rank r with
+// r % 2^(l+1) == 0 absorbs the whole partial of r + 2^l (if < p).
+template <int P>
+__global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
+    const int rank = my_rank(c);
+    const int G = gridDim.x, b = blockIdx.x;
+    const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
+    const bool direct = c.bcast == FC_BCAST_DIRECT;
+    float* own = grad_of(c, rank);
+    bool ok = cta_barrier(c, rank, 0);
+
+    int send_level = -1, last_recv = -1, L = 0;
+    for (int l = 0; (1 << l) < P; ++l, ++L) {
+        if (rank % (2 << l) == 0) {
+            if (rank + (1 << l) < P) last_recv = l;
+        } else if (send_level < 0) {
+            send_level = l;
+        }
+    }
+    const int parent = send_level >= 0 ? rank - (1 << send_level) : -1;
+
+    for (int l = 0; l < L && ok; ++l) {
+        if (rank % (2 << l) != 0) break;  // sent at an earlier level: done reducing
+        const int child = rank + (1 << l);
+        if (child >= P) continue;
+        const bool child_has_children = (l >= 1) && (child + 1 < P);
+        const bool root_final = (rank == 0) && (l == L - 1);
+        const bool signal_parent = (l == last_recv) && (parent >= 0);
+        const float* cg = grad_of(c, child);
+        for (int64_t cc = b; cc < nch; cc += G) {
+            if (child_has_children && !wait_one(c, red_flag(c, rank, l, cc))) { ok = false; break; }
+            reduce_chunk<P>(c, rank, cc, own, cg, root_final, fused, direct);
+            if (signal_parent) signal_one(c, red_flag(c, parent, send_level, cc));
+        }
+    }
+
+    if (!direct) {
+        // receive from the parent at send_level, forward to children at levels send_level-1..0
+        float* mine = fused ? w_of(c, rank) : own;
+        float* dst[3];
+        int nd = 0;
+        const int top = rank == 0 ? L : send_level;
+        for (int l = top - 1; l >= 0; --l)
+            if (rank + (1 << l) < P) dst[nd++] = fused ? w_of(c, rank + (1 << l)) : grad_of(c, rank + (1 << l));
+        for (int64_t cc = b; cc < nch && ok; cc += G) {
+            if (rank != 0 && !wait_one(c, av_flag(c, rank, cc))) { ok = false; break; }
+            if (nd > 0) {
+                copy_chunk(c, cc, mine, dst, nd);
+                __syncthreads();
+                if (threadIdx.x < nd) {
+                    int child = -1, k = 0;
+                    for (int l = top - 1; l >= 0; --l)
+                        if (rank + (1 << l) < P) { if (k == (int)threadIdx.x) child = rank + (1 << l); ++k; }
+                    fence_sys();
+                    st_release_sys(av_flag(c, child, cc), c.epoch);
+                }
+            }
+        }
+    } else {
+        cta_barrier(c, rank, 1);
+    }
+}
+
+// ------------------------------------------------------------ dispatch -----
+template <int P>
+static const void* flat_for(int K) {
+    // K >= P is the same association as K = P (one level, sequential)
+    if (K >= P) K = P;
+    switch (K) {
+        case 2: return (const void*)flat_kernel<P, 2, (P > 4 ? 1 : 2)>;
+#define FC_K(k) case k: if constexpr (P >= k) return (const void*)flat_kernel<P, k, (P > 4 ? 1 : 2)>; else return nullptr;
+        FC_K(3) FC_K(4) FC_K(5) FC_K(6) FC_K(7) FC_K(8)
+#undef FC_K
+    }
+    return nullptr;
+}
+
+template <int P>
+static const void* forest_for() {
+    if constexpr ((P & (P - 1)) == 0) return (const void*)forest_kernel<P>;
+    else return nullptr;
+}
+
+static const void* pick_kernel(int sched, int arity, int p, int op) {
+    if (op == FC_OP_PS) arity = p;
+    switch (p) {
+#define FC_P(PP)                                                                              \
+    case PP:                                                                                  \
+        if (op == FC_OP_PS || sched == FC_SCHED_FLAT) return flat_for<PP>(arity);             \
+        if (sched == FC_SCHED_SINGLE_ROOT) return (const void*)single_root_kernel<PP>;        \
+        return forest_for<PP>();
+        FC_P(2) FC_P(3) FC_P(4) FC_P(5) FC_P(6) FC_P(7) FC_P(8)
+#undef FC_P
+    }
+    return nullptr;
+}
+
+int collective_grid(int sched, int arity, int p, bool virt, bool ps) {
+    const void* fn = pick_kernel(sched, arity, p, ps ? FC_OP_PS : FC_OP_ALLREDUCE);
+    if (!fn) return 0;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TREE_T, 0) != cudaSuccess) return 0;
+    int64_t cap = (int64_t)dev_info().sms * occ;
+    if (virt) cap /= p;
+    if (cap > FC_MAX_CTAS) cap = FC_MAX_CTAS;
+    return (int)cap;
+}
+
+cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
+                              cudaStream_t st) {
+    const void* fn = pick_kernel(sched, arity, c.p, c.op);
+    if (!fn) return cudaErrorInvalidValue;
+    dim3 grid(grid_x, virt ? c.p : 1), block(TREE_T);
+    void* args[] = {(void*)&c};
+    return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
+}
+
+}  // namespace fc

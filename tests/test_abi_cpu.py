@@ -1,0 +1,104 @@
+"""C-ABI library checks that need no GPU (-m "not gpu"): the in-tree
+libfirecaffe.so loads, exports every symbol include/firecaffe.h declares, and
+its host-only helpers behave as documented."""
+import os
+import re
+
+import pytest
+
+import paper_1511_00175_b200 as fc
+from paper_1511_00175_b200 import _lib
+from paper_1511_00175_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    build()
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "firecaffe.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(firecaffe_\w+)\s*\(", src)))
+
+
+def test_every_header_symbol_is_exported_and_bound():
+    names = _header_functions()
+    assert len(names) >= 15
+    L = _lib.load()
+    for n in names:
+        assert hasattr(L, n), n
+        assert n in _lib.SIGNATURES, f"binding lacks {n}"
+    assert set(_lib.SIGNATURES) == set(names)
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_scale_lr_paper_values():
+    # lr 0.01 at batch 256 -> 0.04 at batch 1024
+    assert fc.firecaffe_scale_lr(0.01, 256, 1024) == pytest.approx(0.04, rel=1e-7)
+    assert fc.firecaffe_scale_lr(0.01, 32, 1024) == pytest.approx(0.32, rel=1e-7)
+    assert fc.firecaffe_scale_lr(0.01, 0, 1024) == 0.0
+
+
+def test_status_strings_and_version():
+    assert "timeout" in fc.firecaffe_status_str(_lib.FC_ERR_TIMEOUT)
+    assert fc.firecaffe_status_str(0) == "ok"
+    assert "sm_100a" in fc.firecaffe_version()
+
+
+def test_reserved_prefix_grows_with_heap():
+    a = fc.firecaffe_heap_reserved_bytes(1 << 26)
+    b = fc.firecaffe_heap_reserved_bytes(1 << 33)
+    assert 0 < a < b and a % 65536 == 0 and b % 65536 == 0
+    assert b < (1 << 33) // 100  # flags are < 1 % of the heap
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("n", [0, 1, 4096, 4097, 7_600_000, 143_667_240])
+def test_owned_ranges_partition_the_vector(p, n):
+    for sched in (_lib.FC_SCHED_FOREST, _lib.FC_SCHED_FLAT):
+        ranges = sorted(fc.firecaffe_plan_owned_range(p, sched, r, n) for r in range(p))
+        pos = 0
+        for b, e in ranges:
+            assert b == pos and e >= b
+            pos = e
+        assert pos == n
+        if n >= 4096 * p * 4:  # balanced to within one chunk (+ the ragged last chunk)
+            sizes = [e - b for b, e in ranges]
+            assert max(sizes) - min(sizes) <= 2 * 4096
+    # single root: rank 0 owns everything
+    assert fc.firecaffe_plan_owned_range(p, _lib.FC_SCHED_SINGLE_ROOT, 0, n) == (0, n)
+    assert fc.firecaffe_plan_owned_range(p, _lib.FC_SCHED_SINGLE_ROOT, 1, n) == (0, 0)
+
+
+def test_forest_slices_are_bit_reversed_binomial_roots():
+    # slice index of rank r = bit-reverse(r) (recursive halving keeps the half selected by bit l)
+    n = 8 * 4096 * 10
+    starts = {r: fc.firecaffe_plan_owned_range(8, _lib.FC_SCHED_FOREST, r, n)[0] for r in range(8)}
+    order = sorted(range(8), key=lambda r: starts[r])
+    assert order == [0, 4, 2, 6, 1, 5, 3, 7]
+
+
+def test_host_argument_errors_without_gpu():
+    L = _lib.load()
+    # n < 0 and bad hyper-parameters are rejected before any CUDA call
+    assert L.firecaffe_sgd_step(None, None, None, -1, 0.1, 0.9, 0.0, 1, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_sgd_step(None, None, None, 0, -0.1, 0.9, 0.0, 1, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_sgd_step(None, None, None, 0, 0.1, 1.0, 0.0, 1, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_sgd_step(None, None, None, 0, 0.1, 0.9, -1.0, 1, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_sgd_step(None, None, None, 0, 0.1, 0.9, 0.0, 0, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_sgd_step(None, None, None, 0, 0.1, 0.9, 0.0, 1, None) == _lib.FC_OK  # n == 0 no-op
+    assert L.firecaffe_sgd_step(None, None, None, 8, 0.1, 0.9, 0.0, 1, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_tree_allreduce(None, 4, None, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_world_config(None, 2, 0, 0) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_world_create_virtual(9, 0, None, 1 << 20, 0, None) == _lib.FC_ERR_INVALID_ARG

@@ -1,0 +1,295 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI vs the CPU oracle.
+
+Every comparison is element-by-element and BIT-EXACT (the oracle computes the
+same association and rounding sequence, R1/R6), on seeded inputs
+from fc_inputs (shared generator, no method arithmetic).  Sizes span several
+4096-float chunks plus ragged tails; the multi-rank schedules run in a virtual
+world (p ranks on one GPU, one cooperative kernel) — the same kernels the real
+world launches with one rank per GPU (tests/test_multi_gpu.py).
+"""
+import numpy as np
+import pytest
+import torch
+
+import fc_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+fc = pytest.importorskip("paper_1511_00175_b200")
+
+HYPER = dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024)  # NiN
+SIZES = [1, 3, 4, 5, 4095, 4096, 4097, 3 * 4096 + 7, 100_003, (1 << 20) + 5]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1511_00175_b200.build import build
+
+    build()
+    torch.cuda.set_device(0)
+
+
+def _bits(t):
+    a = t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_bitexact(got, want, what=""):
+    g, w = _bits(got), _bits(want)
+    assert g.shape == w.shape, what
+    bad = np.nonzero(g != w)[0]
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[:5]}: got {g[bad[:3]]} want {w[bad[:3]]}"
+
+
+# ----------------------------------------------------------------- sgd_step --
+@pytest.mark.parametrize("n", [0] + SIZES)
+@pytest.mark.parametrize("zero_mom", [True, False])
+def test_sgd_step_bitexact(n, zero_mom):
+    g = fc_inputs.grad(n, 0, seed=n + 1)
+    w = fc_inputs.weights(n, seed=n + 2)
+    v = fc_inputs.momentum(n, seed=n + 3, zero=zero_mom)
+    wd_, vd = w.cuda(), v.cuda()
+    fc.firecaffe_sgd_step(wd_, g.cuda(), vd, **HYPER)
+    torch.cuda.synchronize()
+    w_ref, v_ref = oracle.sgd(w.numpy(), v.numpy(), g.numpy(), **HYPER)
+    assert_bitexact(wd_, w_ref, "w")
+    assert_bitexact(vd, v_ref, "v")
+
+
+@pytest.mark.parametrize("unroll", [1, 2, 4, 8])
+@pytest.mark.parametrize("dist", ["mixed", "subnormal", "cancel"])
+def test_sgd_step_distributions_and_unroll(unroll, dist):
+    n = 70_001
+    fc.firecaffe_tune_sgd_unroll(unroll)
+    try:
+        g = fc_inputs.grad(n, 1, seed=7, dist=dist)
+        w = fc_inputs.weights(n, seed=8)
+        v = fc_inputs.momentum(n, seed=9)
+        for hp in (HYPER, dict(lr=0.08, mu=0.9, wd=2e-4, batch=1024), dict(lr=0.1, mu=0.0, wd=0.0, batch=3)):
+            wd_, vd = w.cuda(), v.cuda()
+            fc.firecaffe_sgd_step(wd_, g.cuda(), vd, **hp)
+            w_ref, v_ref = oracle.sgd(w.numpy(), v.numpy(), g.numpy(), **hp)
+            assert_bitexact(wd_, w_ref, f"w {hp}")
+            assert_bitexact(vd, v_ref, f"v {hp}")
+    finally:
+        fc.firecaffe_tune_sgd_unroll(4)
+
+
+def test_sgd_step_spec_examples():
+    # SPEC S:89-91 through the GPU: w=1, v=0, g=0.5, lr=0.1, mu=0.9
+    w = torch.tensor([1.0, 1.0, 1.0, 1.0], device="cuda")
+    v = torch.zeros(4, device="cuda")
+    g = torch.full((4,), 0.5, device="cuda")
+    fc.firecaffe_sgd_step(w, g, v, 0.1, 0.9, 0.0, 1)
+    assert_bitexact(w, np.full(4, 0.95, np.float32))
+    fc.firecaffe_sgd_step(w, g, v, 0.1, 0.9, 0.0, 1)
+    assert_bitexact(w, np.full(4, 0.855, np.float32))
+    assert_bitexact(v, np.full(4, 0.095, np.float32))
+
+
+def test_sgd_step_full_nin_size_sampled():
+    """Full NiN size, the launch configuration bench.py times: all elements vs the oracle."""
+    cfg = fc_inputs.CONFIGS["nin"]
+    n = cfg["n"]
+    g = fc_inputs.grad(n, 0, device="cuda")
+    w = fc_inputs.weights(n, device="cuda")
+    v = fc_inputs.momentum(n, device="cuda")
+    gh, wh, vh = g.cpu().numpy(), w.cpu().numpy(), v.cpu().numpy()
+    fc.firecaffe_sgd_step(w, g, v, cfg["lr"], cfg["mu"], cfg["wd"], cfg["batch"])
+    w_ref, v_ref = oracle.sgd(wh, vh, gh, cfg["lr"], cfg["mu"], cfg["wd"], cfg["batch"])
+    assert_bitexact(w, w_ref, "w")
+    assert_bitexact(v, v_ref, "v")
+
+
+def test_sgd_step_rejects_bad_args():
+    x = torch.zeros(8, device="cuda")
+    with pytest.raises(fc.FcError):
+        fc.firecaffe_sgd_step(x, x, x, 0.1, 0.9, 0.0, 1)  # overlapping
+    y, z = torch.zeros(9, device="cuda"), torch.zeros(9, device="cuda")
+    with pytest.raises(fc.FcError):
+        fc.firecaffe_sgd_step(x, y[1:], z[1:], 0.1, 0.9, 0.0, 1, n=8)  # misaligned
+
+
+# ------------------------------------------------------------ virtual world --
+def _world(p, n, bufs=3):
+    from paper_1511_00175_b200.world import heap_bytes_for
+
+    W = fc.World.virtual(p, heap_bytes_for(bufs * max(n, 1) + 64 * bufs))
+    return W
+
+
+def _fill(dst_list, src_rows):
+    for r, t in enumerate(dst_list):
+        t.copy_(src_rows[r])
+
+
+SCHEDS = [("forest", "direct"), ("forest", "tree"), ("single_root", "tree"), ("single_root", "direct"),
+          ("flat", "direct")]
+
+
+def _sched_ok(p, sched):
+    return not (sched == "forest" and (p & (p - 1)) != 0)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("sched,bcast", SCHEDS)
+@pytest.mark.parametrize("n", [1, 4097, 3 * 4096 + 7, 100_003])
+def test_virtual_tree_allreduce_bitexact(p, sched, bcast, n):
+    if not _sched_ok(p, sched):
+        pytest.skip("forest needs a power-of-two world")
+    W = _world(p, n, bufs=1)
+    try:
+        W.config(sched, bcast, 2)
+        grads = W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=1000 + p + n, dist="mixed")
+        _fill(grads, g)
+        fc.firecaffe_tree_allreduce(grads[0], W, n=n)
+        assert W.poll() == 0
+        want = oracle.tree_sum(g.numpy(), 2)
+        for r in range(p):
+            assert_bitexact(grads[r], want, f"rank {r}")
+    finally:
+        W.close()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("sched,bcast", SCHEDS)
+@pytest.mark.parametrize("n", [5, 4096, 3 * 4096 + 7, 100_003])
+def test_virtual_fused_bitexact(p, sched, bcast, n):
+    if not _sched_ok(p, sched):
+        pytest.skip("forest needs a power-of-two world")
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=2000 + p + n)
+        w0 = fc_inputs.weights(n, seed=3)
+        v0 = fc_inputs.momentum(n, seed=4)
+        _fill(grads, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, n=n, **HYPER)
+        assert W.poll() == 0
+        w_ref, v_ref = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **HYPER)
+        covered = np.zeros(n, bool)
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            assert_bitexact(moms[r][b:e], v_ref[b:e], f"mom rank {r} [{b},{e})")
+            covered[b:e] = True
+            # momentum outside the owned slice is untouched (reading R18)
+            m = moms[r].cpu().numpy()
+            keep = np.ones(n, bool)
+            keep[b:e] = False
+            assert_bitexact(m[keep], v0.numpy()[keep], f"untouched mom rank {r}")
+        assert covered.all()
+    finally:
+        W.close()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("n", [7, 4096 * 5 + 1, 100_003])
+def test_virtual_ps_bitexact(p, n):
+    W = _world(p, n, bufs=1)
+    try:
+        grads = W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=3000 + p, dist="mixed")
+        _fill(grads, g)
+        fc.firecaffe_ps_allreduce(grads[0], W, n=n)
+        assert W.poll() == 0
+        want = oracle.ps_sum(g.numpy())
+        for r in range(p):
+            assert_bitexact(grads[r], want, f"rank {r}")
+    finally:
+        W.close()
+
+
+@pytest.mark.parametrize("p,k", [(4, 3), (4, 4), (8, 4), (8, 8), (5, 3), (8, 3), (6, 5)])
+def test_virtual_flat_arity_bitexact(p, k):
+    n = 4096 * 3 + 5
+    W = _world(p, n, bufs=1)
+    try:
+        W.config("flat", "direct", k)
+        grads = W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=4000 + 10 * p + k, dist="mixed")
+        _fill(grads, g)
+        fc.firecaffe_tree_allreduce(grads[0], W, n=n)
+        assert W.poll() == 0
+        want = oracle.tree_sum(g.numpy(), k)
+        for r in range(p):
+            assert_bitexact(grads[r], want, f"rank {r}")
+    finally:
+        W.close()
+
+
+def test_virtual_tiny_config_all_schedules_identical_and_repeatable():
+    """BASELINE configs[0] (tiny: 4 workers, 2^20 floats): every schedule gives the
+    oracle's bits; fused == allreduce + sgd_step; two steps chained; repeat runs equal."""
+    cfg = fc_inputs.CONFIGS["tiny"]
+    n, p = cfg["n"], cfg["p"]
+    hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
+    g = fc_inputs.grads(n, p)
+    w0 = fc_inputs.weights(n)
+    v0 = fc_inputs.momentum(n, zero=True)
+    w1, v1 = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **hp)
+    g2 = fc_inputs.grads(n, p, seed=fc_inputs.SEED + 1)
+    w2, v2 = oracle.fused_step(g2.numpy(), w1, v1, **hp)
+    W = _world(p, n)
+    try:
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        for sched, bcast in SCHEDS:
+            W.config(sched, bcast, 2)
+            _fill(ws, [w0] * p)
+            _fill(moms, [v0] * p)
+            for step, gg, (wr, vr) in ((1, g, (w1, v1)), (2, g2, (w2, v2))):
+                _fill(grads, gg)
+                fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **hp)
+                assert W.poll() == 0
+                for r in range(p):
+                    assert_bitexact(ws[r], wr, f"{sched}/{bcast} step {step} w rank {r}")
+                    b, e = W.owned_range(r, n)
+                    assert_bitexact(moms[r][b:e], vr[b:e], f"{sched}/{bcast} step {step} mom rank {r}")
+        # unfused composition: allreduce then sgd_step on each rank == fused (bitwise)
+        W.config("forest", "tree", 2)
+        _fill(grads, g)
+        fc.firecaffe_tree_allreduce(grads[0], W)
+        for r in range(p):
+            wr_, vr_ = w0.cuda(), v0.cuda()
+            fc.firecaffe_sgd_step(wr_, grads[r], vr_, **hp)
+            assert_bitexact(wr_, w1, f"unfused rank {r}")
+            assert_bitexact(vr_, v1, f"unfused mom rank {r}")
+    finally:
+        W.close()
+
+
+def test_virtual_tolerance_vs_float64():
+    """north_star: within 1e-6 relative (to Σ|g|, reading R15) of a float64 left-to-right sum."""
+    p, n = 8, 200_003
+    W = _world(p, n, bufs=1)
+    try:
+        grads = W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=77, dist="cancel")
+        _fill(grads, g)
+        fc.firecaffe_tree_allreduce(grads[0], W)
+        s = grads[0].cpu().numpy().astype(np.float64)
+        s64 = oracle.sum_f64(g.numpy())
+        a64 = oracle.abs_sum_f64(g.numpy())
+        assert np.all(np.abs(s - s64) <= 1e-6 * a64)
+    finally:
+        W.close()
+
+
+def test_virtual_rejects_non_symmetric_buffers():
+    W = _world(2, 1000, bufs=1)
+    try:
+        outside = torch.zeros(1000, device="cuda")
+        with pytest.raises(fc.FcError) as ei:
+            fc.firecaffe_tree_allreduce(outside, W)
+        assert ei.value.status == 2
+        with pytest.raises(fc.FcError):
+            W.config("forest", "tree", 3)
+    finally:
+        W.close()
