@@ -1,0 +1,492 @@
+#!/usr/bin/env python
+"""Benchmark of the FireCaffe hot path on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config nin]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1)
+    python bench.py --impl reference ...                  (the CPU oracle arm)
+
+A step is one pass of the whole hot path over one batch's gradients:
+  N = 1: firecaffe_sgd_step (the 1-GPU fused SGD, north_star (d)); the tree
+         levels are empty for one worker.
+  N > 1: firecaffe_tree_allreduce_sgd across N real ranks (one process per
+         GPU, peer memory over NVLink): tree reduce + fused SGD + broadcast.
+Workload: BASELINE.json configs[1] (NiN, 7.6M fp32 params, batch 1024) unless
+--config says otherwise.  Inputs are seeded synthetic gradients (fc_inputs).
+The L2 (126 MB) is flushed between timed steps (write + read of 2×512 MB).
+
+value = whole-job algorithm bandwidth: gradient bytes aggregated by all ranks
+(N · 4 · n_params) per second of step time, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tree-allreduce+SGD ms/iter and algo GB/s at 1/2/4/8 B200, % of NVLink/HBM roof"
+GUIDE_NVLINK_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy, per direction per GPU
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="nin")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sched", default=None, help="forest|single_root|flat (default: library default)")
+    ap.add_argument("--bcast", default=None, help="tree|direct")
+    ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--sgd-unroll", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- helpers ---
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus=None):
+        self.proc = None
+        self.lines = []
+        self.gpus = gpus
+
+    def __enter__(self):
+        cmd = ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"]
+        if self.gpus is not None:
+            cmd += ["-i", ",".join(str(g) for g in self.gpus)]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [x for x in sm if x > 500] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(kernel: str, config: str, p: int):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(kernel, {}).get(f"{config}_p{p}")
+    except Exception:
+        return None
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- oracle ----
+def time_oracle(n, p, hp, budget_s=10.0, seed=None):
+    """The CPU oracle as it stands (single thread), on a bounded sample of the
+    workload: the first m elements of every rank's gradient, repeated for about
+    budget_s seconds.  Returns (seconds per element-step, m, steps)."""
+    import numpy as np
+
+    import fc_inputs
+    import oracle
+
+    m = min(n, 1 << 21)
+    g = fc_inputs.grads(m, p).numpy() if p > 1 else fc_inputs.grad(m, 0).numpy()[None, :]
+    w = fc_inputs.weights(m).numpy()
+    v = fc_inputs.momentum(m).numpy()
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        if p > 1:
+            w, v = oracle.fused_step(g, w, v, **hp)
+        else:
+            w, v = oracle.sgd(w, v, g[0], **hp)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    assert np.isfinite(w).all()
+    return el / (steps * m), m, steps
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import fc_inputs
+
+    cfg = fc_inputs.CONFIGS[args.config]
+    n, N = cfg["n"], args.gpus
+    hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
+    # calibrate the per-element cost, then size each step's sample so the whole
+    # warmup+steps run takes about 60 s
+    per_el, _, _ = time_oracle(n, N, hp, budget_s=1.0)
+    total_steps = max(1, args.steps + args.warmup)
+    m = int(max(4096, min(n, 60.0 / (total_steps * per_el))))
+    import numpy as np
+
+    import oracle
+
+    g = fc_inputs.grads(m, N).numpy() if N > 1 else fc_inputs.grad(m, 0).numpy()[None, :]
+    w, v = fc_inputs.weights(m).numpy(), fc_inputs.momentum(m).numpy()
+    ts = []
+    for k in range(total_steps):
+        t0 = time.perf_counter()
+        if N > 1:
+            w, v = oracle.fused_step(g, w, v, **hp)
+        else:
+            w, v = oracle.sgd(w, v, g[0], **hp)
+        if k >= args.warmup:
+            ts.append(time.perf_counter() - t0)
+    assert np.isfinite(w).all()
+    t = sum(ts) / len(ts)
+    value = N * 4 * m / t / 1e9
+    sample = (f"first {m} of {n} params of every rank's gradient per step "
+              f"({'tree sum of %d ranks + ' % N if N > 1 else ''}SGD), single-threaded C++ oracle")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * 1e3 * n / m, 3), "ms_per_step_note": "extrapolated to the full n from the sample",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "n_params": n, "ranks": N, "batch": hp["batch"]},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- ours ------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import fc_inputs
+    import paper_1511_00175_b200 as fc
+    from paper_1511_00175_b200.world import heap_bytes_for
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = world
+    if args.gpus != N:
+        if N == 1 and args.gpus > 1:
+            print(json.dumps({"error": "run N>1 under torchrun"}), flush=True)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    fc.load()
+    if args.sgd_unroll:
+        fc.firecaffe_tune_sgd_unroll(args.sgd_unroll)
+
+    cfg = fc_inputs.CONFIGS[args.config]
+    n = cfg["n"]
+    hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
+    stream = torch.cuda.current_stream()
+    props = torch.cuda.get_device_properties(dev)
+    l2 = getattr(props, "L2_cache_size", 126 << 20)
+
+    # L2 flush buffers: write one, read another (no dirty flush lines left behind)
+    fl_a = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    fl_b = torch.ones(512 << 18, dtype=torch.float32, device=dev)
+
+    def flush():
+        if not args.no_flush:
+            fl_a.zero_()
+            fl_b.sum()
+
+    tiny = torch.zeros(1, device=dev)
+
+    def dev_barrier():
+        if N > 1:
+            dist.all_reduce(tiny)  # device-side rendezvous: kernels start aligned across ranks
+
+    # ---- buffers
+    if N > 1:
+        W = fc.World.create(heap_bytes_for(3 * n + 4096))
+        if args.sched or args.bcast:
+            c = W.get_config()
+            W.config(args.sched or c["sched"], args.bcast or c["bcast"], 2)
+        grad, w, mom = W.alloc(n), W.alloc(n), W.alloc(n)
+    else:
+        W = None
+        grad = torch.empty(n, device=dev)
+        w = torch.empty(n, device=dev)
+        mom = torch.empty(n, device=dev)
+    g0 = fc_inputs.grad(n, rank, device=dev)
+    w0 = fc_inputs.weights(n, device=dev)
+    v0 = fc_inputs.momentum(n, device=dev)
+
+    def reset():
+        grad.copy_(g0)
+        w.copy_(w0)
+        mom.copy_(v0)
+
+    def step():
+        if N > 1:
+            fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, **hp)
+        else:
+            fc.firecaffe_sgd_step(w, grad, mom, **hp)
+
+    # ---- parity spot check (sampled, at full size, in the timed launch configuration)
+    parity = parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W)
+
+    # ---- timed region
+    def timed(fn, K, Wm, pre=None):
+        for _ in range(Wm):
+            if pre:
+                pre()
+            flush()
+            dev_barrier()
+            fn()
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        torch.cuda.synchronize()
+        t_wall0 = time.perf_counter()
+        for k in range(K):
+            if pre:
+                pre()  # restore inputs the previous step consumed (untimed, before the flush)
+            flush()
+            dev_barrier()
+            ev[k][0].record(stream)
+            fn()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        wall = time.perf_counter() - t_wall0
+        ms = [a.elapsed_time(b) for a, b in ev]
+        tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return tot.item() / K, ms, wall
+
+    reset()
+    restore = (lambda: grad.copy_(g0)) if N > 1 else None  # the tree writes partial sums into grad
+    with ClockSampler(gpus=None if N > 1 else [local]) as clk:
+        ms_step, ms_list, wall = timed(step, args.steps, args.warmup, pre=restore)
+    clocks = clk.summary() if rank == 0 else None
+    t = ms_step * 1e-3
+    value = N * 4 * n / t / 1e9
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    g_host = g0.cpu().pin_memory()
+    w_host = torch.empty(n, dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        grad.copy_(g_host, non_blocking=True)
+        step()
+        w_host.copy_(w, non_blocking=True)
+
+    reset()
+    e2e_ms, _, _ = timed(e2e_step, max(5, min(args.steps, 50)), min(args.warmup, 5))
+    e2e_value = N * 4 * n / (e2e_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the only kernel in the step)
+    peaks = measured_peaks()
+    if N == 1:
+        alg_bytes = 20 * n
+        achieved = alg_bytes / t / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": load_traffic("sgd_step_kernel", args.config, 1),
+                "kernel": "fc::sgd_step_kernel", "alg_bytes_per_launch": alg_bytes,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "guide fallback",
+                "frac_of_theoretical_8184": round(achieved / 8184.0, 4)}
+    else:
+        alg_bytes = 2 * (N - 1) / N * 4 * n  # per GPU per direction (allreduce lower bound)
+        achieved = alg_bytes / t / 1e9
+        cfgw = W.get_config()
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": GUIDE_NVLINK_PEER_GBS, "unit": "GB/s",
+                "frac": round(achieved / GUIDE_NVLINK_PEER_GBS, 4),
+                "traffic": load_traffic(f"{cfgw['sched']}_kernel", args.config, N),
+                "kernel": f"fc::{cfgw['sched']}_kernel ({cfgw['bcast']} broadcast)",
+                "alg_bytes_per_launch": alg_bytes,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (nominal 900)",
+                "frac_of_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)}
+
+    # ---- baselines on the same buffers (context: PS, paper's single-root tree, NCCL, torch)
+    baselines = {}
+    if not args.no_baselines:
+        Kb, Wb = max(5, min(args.steps, 50)), min(args.warmup, 5)
+        if N > 1:
+            cur = W.get_config()
+            for sched, bcast in (("forest", "direct"), ("forest", "tree"), ("flat", "direct"),
+                                 ("single_root", "tree"), ("single_root", "direct")):
+                if sched == "forest" and (N & (N - 1)):
+                    continue
+                W.config(sched, bcast, 2)
+                reset()
+                baselines[f"{sched}/{bcast}_ms"] = round(timed(step, Kb, Wb, pre=restore)[0], 4)
+            W.config(cur["sched"], cur["bcast"], cur["arity"])
+
+            def ps_step():
+                fc.firecaffe_ps_allreduce(grad, W)
+                fc.firecaffe_sgd_step(w, grad, mom, **hp)
+
+            def nccl_step():
+                dist.all_reduce(grad)
+                fc.firecaffe_sgd_step(w, grad, mom, **hp)
+
+            reset()
+            baselines["ps+sgd_ms"] = round(timed(ps_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
+            reset()
+            baselines["nccl_allreduce+sgd_ms"] = round(timed(nccl_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
+            baselines["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+        else:
+            def torch_sgd():  # plain PyTorch ops of the same update (several kernels)
+                gg = grad * (1.0 / hp["batch"])
+                gg.add_(w, alpha=hp["wd"])
+                mom.mul_(hp["mu"]).add_(gg, alpha=hp["lr"])
+                w.sub_(mom)
+
+            reset()
+            baselines["torch_eager_sgd_ms"] = round(timed(torch_sgd, Kb, Wb)[0], 4)
+
+    # ---- CPU oracle baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        per_el, m, steps = time_oracle(n, 1, hp, budget_s=10.0)
+        cpu = {"value": round(4 / per_el / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{steps} SGD steps over the first {m} of {n} params (single-threaded C++ oracle)",
+               "ms_per_step_extrapolated": round(per_el * n * 1e3, 3)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s",
+            "value_def": "N*4*n_params bytes of gradient aggregated+applied per second (max over ranks)",
+            "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded N(0,1)*sigma_seg gradients, 64 log-uniform segments; w~N(0,0.01^2))",
+            "config": {"workload": args.config, "n_params": n, "grad_bytes": 4 * n, "ranks": N,
+                       "batch": hp["batch"], "lr": hp["lr"], "mu": hp["mu"], "wd": hp["wd"],
+                       "step": "firecaffe_sgd_step" if N == 1 else "firecaffe_tree_allreduce_sgd",
+                       "schedule": W.get_config() if W else None,
+                       "l2_flush": "no" if args.no_flush else f"write 512 MiB + read 512 MiB between steps (L2 {l2 >> 20} MiB)",
+                       "parallelism": f"dp{N}"},
+            "algbw_gbs": round(4 * n / t / 1e9, 2),
+            "busbw_gbs": round(4 * n / t / 1e9 * 2 * (N - 1) / N, 2) if N > 1 else None,
+            "ms_per_step_median": round(statistics.median(ms_list), 5),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+                    "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_ms, 4),
+                    "what": "pinned host grad -> device, the step, updated w -> pinned host"},
+            "gpu_launches": args.steps,
+            "gpu_launches_note": "one library kernel per step (L2-flush and barrier kernels are torch/NCCL)",
+            "clocks": clocks,
+            "parity": parity,
+            "baselines_ms_per_step": baselines,
+            "wall_s_timed_region": round(wall, 3),
+        }
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W):
+    """One step at full size, compared with the oracle on 8192 sampled indices
+    (all ranks' inputs gathered for those indices), plus a cross-rank digest."""
+    import numpy as np
+
+    import oracle
+
+    reset()
+    step()
+    torch.cuda.synchronize()
+    gen = torch.Generator().manual_seed(12345)
+    idx = torch.randint(0, n, (8192,), generator=gen)
+    idx = torch.cat([idx, torch.arange(max(0, n - 64), n)])  # include the ragged tail
+    idx_d = idx.to(grad.device)
+    gs = g0[idx_d].contiguous()
+    if N > 1:
+        allg = [torch.empty_like(gs) for _ in range(N)]
+        dist.all_gather(allg, gs)
+        G = torch.stack(allg).cpu().numpy()
+    else:
+        G = gs.cpu().numpy()[None, :]
+    w_ref, v_ref = oracle.fused_step(G, w0[idx_d].cpu().numpy(), v0[idx_d].cpu().numpy(), **hp) if N > 1 else \
+        oracle.sgd(w0[idx_d].cpu().numpy(), v0[idx_d].cpu().numpy(), G[0], **hp)
+    w_got = w[idx_d].cpu().numpy()
+    ok_w = bool(np.array_equal(w_got.view(np.uint32), w_ref.view(np.uint32)))
+    # momentum: compare on the indices this rank owns
+    if N > 1:
+        b, e = W.owned_range(rank, n)
+    else:
+        b, e = 0, n
+    own = (idx >= b) & (idx < e)
+    ok_v = bool(np.array_equal(mom[idx_d].cpu().numpy()[own.numpy()].view(np.uint32),
+                               v_ref[own.numpy()].view(np.uint32)))
+    digest = int(w.view(torch.int32).to(torch.int64).sum().item() % (1 << 61))
+    ok = torch.tensor([1 if (ok_w and ok_v) else 0], device=grad.device)
+    dg = torch.tensor([digest], dtype=torch.int64, device=grad.device)
+    same = True
+    if N > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        dmin, dmax = dg.clone(), dg.clone()
+        dist.all_reduce(dmin, op=dist.ReduceOp.MIN)
+        dist.all_reduce(dmax, op=dist.ReduceOp.MAX)
+        same = dmin.item() == dmax.item()
+    status = W.poll() if W is not None else 0
+    return {"bitexact_sampled": bool(ok.item() == 1), "samples": int(idx.numel()), "ranks_identical_digest": same,
+            "device_status": status}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

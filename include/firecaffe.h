@@ -200,6 +200,14 @@ float firecaffe_scale_lr(float base_lr, int64_t base_batch, int64_t batch);
 
 const char* firecaffe_status_str(fc_status s);
 
+/* Diagnostics: when `buf` (device memory, `capacity` uint64 words) is set, every
+ * collective kernel writes four %globaltimer stamps per CTA (entry, after the
+ * entry barrier, after the data phase, exit) to buf[(vrank*grid + cta)*4 + slot]
+ * (vrank = 0 in a real world).  Pass NULL to disable.  Value-neutral.
+ * firecaffe_world_last_grid returns the CTAs per rank of the last collective. */
+fc_status firecaffe_world_set_trace(fc_world* world, uint64_t* buf, int64_t capacity);
+int firecaffe_world_last_grid(const fc_world* world);
+
 /* Tuning knob for firecaffe_sgd_step: float4s in flight per thread per operand
  * (1, 2, 4 or 8; default 4).  Process-wide; value-neutral. */
 void firecaffe_tune_sgd_unroll(int unroll);

@@ -54,6 +54,8 @@ SIGNATURES = {
     "firecaffe_scale_lr": (_F, [_F, _I64, _I64]),
     "firecaffe_status_str": (ctypes.c_char_p, [_I]),
     "firecaffe_tune_sgd_unroll": (None, [_I]),
+    "firecaffe_world_set_trace": (_I, [_P, _P, _I64]),
+    "firecaffe_world_last_grid": (_I, [_P]),
     "firecaffe_version": (ctypes.c_char_p, []),
 }
 

@@ -28,6 +28,9 @@ struct fc_world {
     fc_sched sched;
     fc_bcast bcast;
     FcFlagLayout layout;
+    uint64_t* trace;
+    int64_t trace_cap;
+    int last_grid;
 };
 
 namespace fc {
@@ -351,6 +354,9 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     const int sched = op == FC_OP_PS ? FC_SCHED_FLAT : w->sched;
     const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op == FC_OP_PS);
     if (grid < 1) return FC_ERR_UNSUPPORTED;
+    w->last_grid = grid;
+    const int64_t need = (int64_t)grid * (w->virt ? w->p : 1) * FC_TRACE_SLOTS;
+    c.trace = (w->trace && w->trace_cap >= need) ? w->trace : nullptr;
     cudaError_t e = launch_collective(c, sched, w->arity, w->virt != 0, grid, (cudaStream_t)stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -390,5 +396,14 @@ fc_status firecaffe_tree_allreduce_sgd(float* wt, float* grad, float* mom, int64
 }
 
 void firecaffe_tune_sgd_unroll(int u) { set_sgd_unroll(u); }
+
+fc_status firecaffe_world_set_trace(fc_world* w, uint64_t* buf, int64_t capacity) {
+    if (!w || capacity < 0) return FC_ERR_INVALID_ARG;
+    w->trace = buf;
+    w->trace_cap = buf ? capacity : 0;
+    return FC_OK;
+}
+
+int firecaffe_world_last_grid(const fc_world* w) { return w ? w->last_grid : 0; }
 
 }  // extern "C"

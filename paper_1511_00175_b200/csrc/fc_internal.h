@@ -54,6 +54,9 @@ struct FcColl {
     float lr, mu, wd, inv_b;
     int bcast;         // fc_bcast
     int64_t bar_words, red_words, max_chunks;
+    uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]
 };
+
+#define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit
 
 enum FcOp { FC_OP_ALLREDUCE = 0, FC_OP_ALLREDUCE_SGD = 1, FC_OP_PS = 2 };

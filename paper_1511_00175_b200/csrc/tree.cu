@@ -60,6 +60,11 @@ __device__ __forceinline__ float* mom_of(const FcColl& c, int q) {
     return c.off_mom >= 0 ? reinterpret_cast<float*>(c.peers.heap[q] + c.off_mom) : c.mom_local;
 }
 
+__device__ __forceinline__ void trace(const FcColl& c, int slot) {
+    if (c.trace && threadIdx.x == 0)
+        c.trace[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * FC_TRACE_SLOTS + slot] = globaltimer();
+}
+
 // ------------------------------------------------------------ sync ---------
 // All-to-all barrier among the CTAs with this blockIdx.x on every rank
 // (slot 0 = entry, 1 = exit).  Thread q < p pushes "rank arrived" into rank q's
@@ -229,7 +234,9 @@ __device__ __forceinline__ void copy_chunk(const FcColl& c, int64_t cc, const fl
 template <int P, int K, int U>
 __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
     const int rank = my_rank(c);
+    trace(c, 0);
     const bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
     if (ok) {
         const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
         int64_t c0, c1;
@@ -309,7 +316,9 @@ __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
             }
         }
     }
+    trace(c, 2);
     cta_barrier(c, rank, 1);
+    trace(c, 3);
 }
 
 // ------------------------------------------------------------ FOREST -------
@@ -323,7 +332,9 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
     const bool direct = c.bcast == FC_BCAST_DIRECT;
     float* own = grad_of(c, rank);
+    trace(c, 0);
     bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
 
     // ---- reduce: recursive halving, level l pairs rank with rank ^ 2^l
     int64_t lo = 0, hi = nch;
@@ -344,6 +355,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     }
 
     // ---- broadcast back down the tree (recursive doubling), or direct
+    trace(c, 2);
     if (!direct) {
         const int64_t o0 = lo, o1 = hi;  // owned slice
         float* mine = fused ? w_of(c, rank) : own;
@@ -373,6 +385,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     } else {
         cta_barrier(c, rank, 1);
     }
+    trace(c, 3);
 }
 
 // ------------------------------------------------------------ SINGLE ROOT --
@@ -386,7 +399,9 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
     const bool direct = c.bcast == FC_BCAST_DIRECT;
     float* own = grad_of(c, rank);
+    trace(c, 0);
     bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
 
     int send_level = -1, last_recv = -1, L = 0;
     for (int l = 0; (1 << l) < P; ++l, ++L) {
@@ -413,6 +428,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         }
     }
 
+    trace(c, 2);
     if (!direct) {
         // receive from the parent at send_level, forward to children at levels send_level-1..0
         float* mine = fused ? w_of(c, rank) : own;
@@ -438,6 +454,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
     } else {
         cta_barrier(c, rank, 1);
     }
+    trace(c, 3);
 }
 
 // ------------------------------------------------------------ dispatch -----

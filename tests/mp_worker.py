@@ -1,0 +1,109 @@
+"""Worker for tests/test_multi_gpu.py: run under torchrun, one process per GPU.
+
+Real world (CUDA IPC heaps, NVLink peer memory): every schedule / broadcast /
+op is compared bit-exactly with the CPU oracle (each rank checks its own
+result; rank 0 gathers all inputs), the cross-rank digest must agree, and a
+final check makes rank 1 skip a collective so rank 0 must report
+FC_ERR_TIMEOUT instead of hanging.  Prints "MP_OK <rank>" on success.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import fc_inputs  # noqa: E402
+import oracle  # noqa: E402
+import paper_1511_00175_b200 as fc  # noqa: E402
+from paper_1511_00175_b200.world import heap_bytes_for  # noqa: E402
+
+HP = dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024)
+
+
+def bits(t):
+    return np.ascontiguousarray(t.detach().cpu().numpy(), np.float32).view(np.uint32)
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    rank, p = dist.get_rank(), dist.get_world_size()
+    sizes = [int(s) for s in os.environ.get("FC_MP_SIZES", "5,16391,1000003").split(",")]
+    nmax = max(sizes)
+    W = fc.World.create(heap_bytes_for(3 * nmax + 4096), timeout_s=float(os.environ.get("FC_MP_TIMEOUT", "20")))
+    grad, w, mom = W.alloc(nmax), W.alloc(nmax), W.alloc(nmax)
+    scheds = [("forest", "direct"), ("forest", "tree"), ("flat", "direct"), ("single_root", "tree"),
+              ("single_root", "direct")]
+    if p & (p - 1):
+        scheds = [s for s in scheds if s[0] != "forest"]
+    fails = []
+    for n in sizes:
+        g_all = fc_inputs.grads(n, p, seed=5000 + n)  # every rank can rebuild every input (seeded)
+        w0, v0 = fc_inputs.weights(n, seed=6), fc_inputs.momentum(n, seed=7)
+        s_ref = oracle.tree_sum(g_all.numpy(), 2)
+        w_ref, v_ref = oracle.sgd(w0.numpy(), v0.numpy(), s_ref, **HP)
+        ps_ref = oracle.ps_sum(g_all.numpy())
+        for sched, bcast in scheds:
+            W.config(sched, bcast, 2)
+            # allreduce
+            grad[:n].copy_(g_all[rank])
+            fc.firecaffe_tree_allreduce(grad, W, n=n)
+            torch.cuda.synchronize()
+            if not np.array_equal(bits(grad[:n]), s_ref.view(np.uint32)):
+                fails.append(f"allreduce {sched}/{bcast} n={n}")
+            # fused
+            grad[:n].copy_(g_all[rank])
+            w[:n].copy_(w0)
+            mom[:n].copy_(v0)
+            fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, n=n, **HP)
+            torch.cuda.synchronize()
+            if not np.array_equal(bits(w[:n]), w_ref.view(np.uint32)):
+                fails.append(f"fused w {sched}/{bcast} n={n}")
+            b, e = W.owned_range(rank, n)
+            if not np.array_equal(bits(mom[b:e]), v_ref[b:e].view(np.uint32)):
+                fails.append(f"fused mom {sched}/{bcast} n={n}")
+        # parameter server
+        grad[:n].copy_(g_all[rank])
+        fc.firecaffe_ps_allreduce(grad, W, n=n)
+        torch.cuda.synchronize()
+        if not np.array_equal(bits(grad[:n]), ps_ref.view(np.uint32)):
+            fails.append(f"ps n={n}")
+    st = W.poll()
+    if st != 0:
+        fails.append(f"device status {st}")
+    # all ranks hold identical weights
+    dg = torch.tensor([int(w[:nmax].view(torch.int32).to(torch.int64).sum().item())], device=dev)
+    lo, hi = dg.clone(), dg.clone()
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    if lo.item() != hi.item():
+        fails.append("digest differs across ranks")
+    nf = torch.tensor([len(fails)], device=dev)
+    dist.all_reduce(nf)
+    if fails:
+        print(f"rank {rank} FAILS: {fails}", flush=True)
+    if nf.item() == 0 and os.environ.get("FC_MP_TIMEOUT_TEST", "1") == "1":
+        # fault test: rank 1 never arrives -> the others time out (no hang)
+        dist.barrier()
+        if rank != 1:
+            grad[:1000].copy_(g_all[rank][:1000]) if sizes[-1] >= 1000 else None
+            fc.firecaffe_tree_allreduce(grad, W, n=1000)
+            st = W.poll()
+            if st != 4:
+                print(f"rank {rank} expected FC_ERR_TIMEOUT, got {st}", flush=True)
+                nf += 1
+        dist.barrier()
+    if nf.item() == 0:
+        print(f"MP_OK {rank}", flush=True)
+    dist.destroy_process_group()
+    return 0 if nf.item() == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

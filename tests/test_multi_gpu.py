@@ -1,0 +1,29 @@
+"""Real multi-GPU parity (-m gpu; needs >= 2 GPUs, skipped otherwise).
+
+Launches tests/mp_worker.py under torchrun with one process per GPU: CUDA-IPC
+heaps, NVLink peer loads/stores, every schedule bit-exact vs the oracle, all
+ranks bit-identical, and a missing rank yields FC_ERR_TIMEOUT instead of a hang.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_real_world_parity(nproc):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    env = dict(os.environ, FC_MP_TIMEOUT="5", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29600 + nproc}", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    for k in range(nproc):
+        assert f"MP_OK {k}" in out, out[-4000:]
