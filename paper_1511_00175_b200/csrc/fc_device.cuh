@@ -69,6 +69,14 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -82,17 +90,22 @@ __device__ __forceinline__ bool reached(uint32_t flag, uint32_t epoch) {
     return (int32_t)(flag - epoch) >= 0;
 }
 
-// Spin until *f has reached `epoch`.  Bounded by timeout_ns of %globaltimer;
-// on timeout records FC_ERR_TIMEOUT in *status and returns false.  Also gives
-// up immediately once any CTA has recorded an error (so one missing peer does
-// not cost one timeout per wait).
+// Spin until *f has reached `epoch`.  Polls with relaxed sys-scope loads and
+// performs ONE acquire load once the stamp is seen (acquire: later loads of
+// the producer's data cannot be satisfied before the flag).  Bounded by
+// timeout_ns of %globaltimer; on timeout records FC_ERR_TIMEOUT in *status
+// and returns false.  Also gives up once any CTA has recorded an error (so one
+// missing peer does not cost one timeout per wait).
 __device__ __forceinline__ bool wait_flag(const uint32_t* f, uint32_t epoch, uint64_t timeout_ns,
                                           int* status) {
     if (reached(ld_acquire_sys(f), epoch)) return true;
     const uint64_t t0 = globaltimer();
     uint32_t spins = 0;
     while (true) {
-        if (reached(ld_acquire_sys(f), epoch)) return true;
+        if (reached(ld_relaxed_sys(f), epoch)) {
+            (void)ld_acquire_sys(f);
+            return true;
+        }
         if ((++spins & 63u) == 0) {
             if (*(volatile int*)status != FC_OK) return false;
             if (globaltimer() - t0 > timeout_ns) {

@@ -22,6 +22,8 @@
 // by CTA cc % gridDim.x, element k of a chunk always by the same thread, so a
 // rank's own partial sums need no flags between levels (program order).
 #include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "fc_device.cuh"
 #include "fc_launch.h"
@@ -68,16 +70,21 @@ __device__ __forceinline__ void trace(const FcColl& c, int slot) {
 // ------------------------------------------------------------ sync ---------
 // All-to-all barrier among the CTAs with this blockIdx.x on every rank
 // (slot 0 = entry, 1 = exit).  Thread q < p pushes "rank arrived" into rank q's
-// heap, then spins on rank q's stamp in the local heap.  The fence orders the
-// CTA's earlier writes (peer stores included; the caller's __syncthreads
-// orders the other threads' writes before it) ahead of the flag.
+// heap, then spins on rank q's stamp in the local heap.
+//  entry (slot 0): the stamp orders nothing the CTA wrote (the rank's inputs
+//    were produced by earlier kernels, complete and coherent in its L2), so it
+//    is a relaxed store: no fence on the critical path.
+//  exit (slot 1): st.release.sys orders the CTA's earlier writes — peer stores
+//    included; the __syncthreads orders the other threads' writes before it
+//    (PTX causality through bar.sync) — ahead of the stamp.
 __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
     __syncthreads();
     const int t = threadIdx.x;
     bool good = true;
     if (t < c.p && t != rank) {
-        fence_sys();
-        st_release_sys(bar_flag(c, t, slot, blockIdx.x, rank), c.epoch);
+        uint32_t* dst = bar_flag(c, t, slot, blockIdx.x, rank);
+        if (slot == 0) st_relaxed_sys(dst, c.epoch);
+        else st_release_sys(dst, c.epoch);
         good = wait_flag(bar_flag(c, rank, slot, blockIdx.x, t), c.epoch, c.timeout_ns, c.status);
     }
     return __syncthreads_and(good) != 0;
@@ -93,10 +100,7 @@ __device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
 // After the CTA finished writing a chunk: publish it with one flag.
 __device__ __forceinline__ void signal_one(const FcColl& c, uint32_t* f) {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        fence_sys();
-        st_release_sys(f, c.epoch);
-    }
+    if (threadIdx.x == 0) st_release_sys(f, c.epoch);
 }
 
 __device__ __forceinline__ int64_t first_chunk(int64_t lo, int G, int b) {
@@ -446,7 +450,6 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
                     int child = -1, k = 0;
                     for (int l = top - 1; l >= 0; --l)
                         if (rank + (1 << l) < P) { if (k == (int)threadIdx.x) child = rank + (1 << l); ++k; }
-                    fence_sys();
                     st_release_sys(av_flag(c, child, cc), c.epoch);
                 }
             }
@@ -508,7 +511,18 @@ cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, 
     if (!fn) return cudaErrorInvalidValue;
     dim3 grid(grid_x, virt ? c.p : 1), block(TREE_T);
     void* args[] = {(void*)&c};
-    return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
+    // A virtual world's CTAs wait on CTAs of the same launch: they must be
+    // co-resident, which only a cooperative launch guarantees.  In a real world
+    // CTA b only ever waits on CTA b of OTHER GPUs and the grid never exceeds one
+    // resident wave, so a plain launch suffices (and starts sooner);
+    // FC_LAUNCH=coop forces the cooperative path for diagnosis.
+    static int force_coop = -1;
+    if (force_coop < 0) {
+        const char* e = getenv("FC_LAUNCH");
+        force_coop = (e && strcmp(e, "coop") == 0) ? 1 : 0;
+    }
+    if (virt || force_coop) return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
+    return cudaLaunchKernel(fn, grid, block, args, 0, st);
 }
 
 }  // namespace fc
