@@ -252,6 +252,10 @@ def main():
     def dev_barrier():
         if N > 1:
             dist.all_reduce(tiny)  # device-side rendezvous: kernels start aligned across ranks
+            # ~20 us of GPU-side delay, equal on every rank (same clock): the host has
+            # enqueued the timed kernel before the GPU reaches the start event, as in a
+            # training loop where the allreduce is queued behind the backward pass
+            torch.cuda._sleep(40_000)
 
     # ---- buffers
     if N > 1:

@@ -30,7 +30,11 @@
 
 namespace fc {
 
-constexpr int TREE_T = 256;                       // threads per CTA
+constexpr int TREE_T = 256;                       // threads per CTA (tree schedules)
+constexpr int FLAT_T = 512;                       // threads per CTA (FLAT / PS), one CTA per SM
+// float4 per thread per operand in flight in FLAT: enough remote bytes in flight
+// (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
+#define FLAT_UNROLL(P) ((P) <= 3 ? 2 : 1)
 constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
 constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
 static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
@@ -236,7 +240,7 @@ __device__ __forceinline__ void copy_chunk(const FcColl& c, int64_t cc, const fl
 // server's sequential order), then either applies SGD and pushes w' to every
 // rank (fused) or pushes the sum to every rank's grad.
 template <int P, int K, int U>
-__global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
+__global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     const int rank = my_rank(c);
     trace(c, 0);
     const bool ok = cta_barrier(c, rank, 0);
@@ -250,15 +254,19 @@ __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
         const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
         if (e1 > e0) {
             const int64_t i0 = e0 / 4, i1 = e1 / 4;
-            const int64_t T = TREE_T;
+            const int64_t T = FLAT_T;
+            // grid-stride: all CTAs sweep the slice in lockstep, so at any moment the
+            // GPU's remote reads fall in one few-MB window of each peer's heap (a
+            // contiguous range per CTA measured ~10% slower: 444 scattered streams)
+            const int64_t ce = i1;
             const int64_t stride = (int64_t)gridDim.x * T * U;
-            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < i1;
+            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < ce;
                  base += stride) {
                 float4 x[U][P];
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
                     const int64_t i = base + j * T;
-                    if (i < i1) {
+                    if (i < ce) {
 #pragma unroll
                         for (int q = 0; q < P; ++q)
                             x[j][q] = ld_cg(reinterpret_cast<const float4*>(grad_of(c, q)) + i);
@@ -271,7 +279,7 @@ __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const int64_t i = base + j * T;
-                        if (i < i1) {
+                        if (i < ce) {
                             w[j] = ld_rw(w4 + i);
                             v[j] = ld_rw(v4 + i);
                         }
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const int64_t i = base + j * T;
-                        if (i < i1) {
+                        if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
                             sgd4(S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
                             st_na(v4 + i, v[j]);
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(TREE_T) flat_kernel(const FcColl c) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const int64_t i = base + j * T;
-                        if (i < i1) {
+                        if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
 #pragma unroll
                             for (int q = 0; q < P; ++q)
@@ -465,9 +473,10 @@ template <int P>
 static const void* flat_for(int K) {
     // K >= P is the same association as K = P (one level, sequential)
     if (K >= P) K = P;
+    constexpr int U = FLAT_UNROLL(P);
     switch (K) {
-        case 2: return (const void*)flat_kernel<P, 2, (P > 4 ? 1 : 2)>;
-#define FC_K(k) case k: if constexpr (P >= k) return (const void*)flat_kernel<P, k, (P > 4 ? 1 : 2)>; else return nullptr;
+        case 2: return (const void*)flat_kernel<P, 2, U>;
+#define FC_K(k) case k: if constexpr (P >= k) return (const void*)flat_kernel<P, k, U>; else return nullptr;
         FC_K(3) FC_K(4) FC_K(5) FC_K(6) FC_K(7) FC_K(8)
 #undef FC_K
     }
@@ -480,49 +489,75 @@ static const void* forest_for() {
     else return nullptr;
 }
 
-static const void* pick_kernel(int sched, int arity, int p, int op) {
+struct KernelPick {
+    const void* fn;
+    int block;
+    bool flat;
+};
+
+static KernelPick pick_kernel(int sched, int arity, int p, int op) {
     if (op == FC_OP_PS) arity = p;
+    const bool flat = op == FC_OP_PS || sched == FC_SCHED_FLAT;
+    KernelPick k{nullptr, flat ? FLAT_T : TREE_T, flat};
     switch (p) {
 #define FC_P(PP)                                                                              \
     case PP:                                                                                  \
-        if (op == FC_OP_PS || sched == FC_SCHED_FLAT) return flat_for<PP>(arity);             \
-        if (sched == FC_SCHED_SINGLE_ROOT) return (const void*)single_root_kernel<PP>;        \
-        return forest_for<PP>();
+        if (flat) k.fn = flat_for<PP>(arity);                                                 \
+        else if (sched == FC_SCHED_SINGLE_ROOT) k.fn = (const void*)single_root_kernel<PP>;   \
+        else k.fn = forest_for<PP>();                                                         \
+        break;
         FC_P(2) FC_P(3) FC_P(4) FC_P(5) FC_P(6) FC_P(7) FC_P(8)
 #undef FC_P
     }
-    return nullptr;
+    return k;
 }
 
+// CTAs per rank.  FLAT: one wide CTA per SM — every CTA pays a sys-scope
+// release fence at the exit barrier and that fence gets slower with the number
+// of CTAs issuing it (4.4 us at 148 CTAs, 7.8 us at 444; scripts/fence_bench.cu,
+// launch_bench.cu).  Tree schedules: as many 256-thread CTAs as fit (their
+// chunk pipeline wants more independent CTAs).  Virtual worlds share one GPU.
 int collective_grid(int sched, int arity, int p, bool virt, bool ps) {
-    const void* fn = pick_kernel(sched, arity, p, ps ? FC_OP_PS : FC_OP_ALLREDUCE);
-    if (!fn) return 0;
+    const KernelPick k = pick_kernel(sched, arity, p, ps ? FC_OP_PS : FC_OP_ALLREDUCE);
+    if (!k.fn) return 0;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, TREE_T, 0) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.block, 0) != cudaSuccess) return 0;
+    if (occ < 1) return 0;
+    static int flat_per_sm = -1;
+    if (flat_per_sm < 0) {
+        const char* e = getenv("FC_FLAT_CTAS_PER_SM");
+        flat_per_sm = e ? atoi(e) : 1;
+        if (flat_per_sm < 1) flat_per_sm = 1;
+    }
+    if (k.flat && occ > flat_per_sm) occ = flat_per_sm;
     int64_t cap = (int64_t)dev_info().sms * occ;
-    if (virt) cap /= p;
+    if (virt) {
+        int occ_all = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_all, k.fn, k.block, 0);
+        cap = (int64_t)dev_info().sms * occ_all / p;
+    }
     if (cap > FC_MAX_CTAS) cap = FC_MAX_CTAS;
     return (int)cap;
 }
 
 cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
                               cudaStream_t st) {
-    const void* fn = pick_kernel(sched, arity, c.p, c.op);
-    if (!fn) return cudaErrorInvalidValue;
-    dim3 grid(grid_x, virt ? c.p : 1), block(TREE_T);
+    const KernelPick k = pick_kernel(sched, arity, c.p, c.op);
+    if (!k.fn) return cudaErrorInvalidValue;
+    dim3 grid(grid_x, virt ? c.p : 1), block(k.block);
     void* args[] = {(void*)&c};
     // A virtual world's CTAs wait on CTAs of the same launch: they must be
     // co-resident, which only a cooperative launch guarantees.  In a real world
     // CTA b only ever waits on CTA b of OTHER GPUs and the grid never exceeds one
-    // resident wave, so a plain launch suffices (and starts sooner);
+    // resident wave, so a plain launch suffices;
     // FC_LAUNCH=coop forces the cooperative path for diagnosis.
     static int force_coop = -1;
     if (force_coop < 0) {
         const char* e = getenv("FC_LAUNCH");
         force_coop = (e && strcmp(e, "coop") == 0) ? 1 : 0;
     }
-    if (virt || force_coop) return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st);
-    return cudaLaunchKernel(fn, grid, block, args, 0, st);
+    if (virt || force_coop) return cudaLaunchCooperativeKernel(k.fn, grid, block, args, 0, st);
+    return cudaLaunchKernel(k.fn, grid, block, args, 0, st);
 }
 
 }  // namespace fc

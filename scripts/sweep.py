@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--scheds", default="forest/direct,forest/tree,flat/direct,single_root/tree,single_root/direct")
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--nccl", action="store_true")
+    ap.add_argument("--sleep", type=int, default=40000, help="GPU cycles of delay after the rendezvous")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -71,6 +72,8 @@ def main():
                     fl_a.zero_()
                     fl_b.sum()
                     dist.all_reduce(tiny)
+                    if args.sleep:
+                        torch.cuda._sleep(args.sleep)  # host runs ahead of the GPU (see bench.py)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record()
                     if op == "fused" and sched == "nccl":
