@@ -53,8 +53,64 @@ def parse():
 
 
 # ---------------------------------------------------------------- helpers ---
+class NvmlClockSampler:
+    """SM clock and clock-event (throttle) reasons polled through NVML every
+    ~2 ms on a thread, for the whole timed region (which can be well under a
+    second, too short for nvidia-smi's 100 ms loop)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, gpus):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.handles = [pynvml.nvmlDeviceGetHandleByIndex(g) for g in gpus]
+        self.sm, self.reasons, self.smax = [], set(), 0
+        self.stop = threading.Event()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            for h in self.handles:
+                try:
+                    self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    self.smax = max(self.smax, nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for k, bit in self.REASONS.items():
+                        if mask & bit:
+                            self.reasons.add(k)
+                except Exception:
+                    pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        time.sleep(0.01)
+        return self
+
+    def __exit__(self, *a):
+        time.sleep(0.01)
+        self.stop.set()
+        self.t.join(timeout=5)
+
+    def summary(self):
+        busy = [x for x in self.sm if x > 500] or self.sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": self.smax or None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
+
+
+def clock_sampler(gpus):
+    try:
+        return NvmlClockSampler(gpus)
+    except Exception:
+        return ClockSampler(gpus)
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """Fallback: nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
     Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -321,7 +377,7 @@ def main():
 
     reset()
     restore = (lambda: grad.copy_(g0)) if N > 1 else None  # the tree writes partial sums into grad
-    with ClockSampler(gpus=None if N > 1 else [local]) as clk:
+    with clock_sampler(list(range(N)) if (N > 1 and rank == 0) else [local]) as clk:
         ms_step, ms_list, wall = timed(step, args.steps, args.warmup, pre=restore)
     clocks = clk.summary() if rank == 0 else None
     t = ms_step * 1e-3

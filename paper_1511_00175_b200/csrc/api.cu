@@ -353,7 +353,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.red_words = w->layout.red_words;
     c.max_chunks = w->layout.max_chunks;
     const int sched = op == FC_OP_PS ? FC_SCHED_FLAT : w->sched;
-    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op == FC_OP_PS);
+    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op == FC_OP_PS, n);
     if (grid < 1) return FC_ERR_UNSUPPORTED;
     w->last_grid = grid;
     const int64_t need = (int64_t)grid * (w->virt ? w->p : 1) * FC_TRACE_SLOTS;

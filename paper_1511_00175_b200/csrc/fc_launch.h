@@ -21,7 +21,7 @@ void set_sgd_unroll(int u);
 cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
                               cudaStream_t st);
 // Max CTAs per rank that can be co-resident for this schedule (virt: divided by p).
-int collective_grid(int sched, int arity, int p, bool virt, bool ps);
+int collective_grid(int sched, int arity, int p, bool virt, bool ps, int64_t n);
 
 // Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
 __host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }

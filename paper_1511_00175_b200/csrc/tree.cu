@@ -517,19 +517,24 @@ static KernelPick pick_kernel(int sched, int arity, int p, int op) {
 // of CTAs issuing it (4.4 us at 148 CTAs, 7.8 us at 444; scripts/fence_bench.cu,
 // launch_bench.cu).  Tree schedules: as many 256-thread CTAs as fit (their
 // chunk pipeline wants more independent CTAs).  Virtual worlds share one GPU.
-int collective_grid(int sched, int arity, int p, bool virt, bool ps) {
+int collective_grid(int sched, int arity, int p, bool virt, bool ps, int64_t n) {
     const KernelPick k = pick_kernel(sched, arity, p, ps ? FC_OP_PS : FC_OP_ALLREDUCE);
-    if (!k.fn) return 0;
+    if (!k.fn || p < 1) return 0;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.block, 0) != cudaSuccess) return 0;
     if (occ < 1) return 0;
     static int flat_per_sm = -1;
     if (flat_per_sm < 0) {
         const char* e = getenv("FC_FLAT_CTAS_PER_SM");
-        flat_per_sm = e ? atoi(e) : 1;
-        if (flat_per_sm < 1) flat_per_sm = 1;
+        flat_per_sm = e ? atoi(e) : 0;  // 0 = by size
     }
-    if (k.flat && occ > flat_per_sm) occ = flat_per_sm;
+    if (k.flat) {
+        // measured (p = 2, 4): 1 CTA/SM wins while the per-rank slice is small (the
+        // fixed exit cost dominates), 2 CTAs/SM from ~32 MB slices on (more bytes in
+        // flight): NiN p=2 63.5 vs 66.6 us, VGG-19 p=2 932 vs 879 us
+        int want = flat_per_sm > 0 ? flat_per_sm : (n / p >= (int64_t)(8 << 20) ? 2 : 1);
+        if (occ > want) occ = want;
+    }
     int64_t cap = (int64_t)dev_info().sms * occ;
     if (virt) {
         int occ_all = 0;
