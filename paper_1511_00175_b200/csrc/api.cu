@@ -344,6 +344,26 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.rank = w->virt ? -1 : w->rank;
     c.p = w->p;
     c.epoch = ++w->epoch;
+    {  // call signature (FNV-1a): every rank must make the same call
+        uint32_t h = 2166136261u;
+        auto mix = [&h](const void* p, size_t len) {
+            const unsigned char* b = (const unsigned char*)p;
+            for (size_t i = 0; i < len; ++i) h = (h ^ b[i]) * 16777619u;
+        };
+        const int sched_used = op == FC_OP_PS ? -1 : (int)w->sched;
+        const int bc = (int)w->bcast;
+        mix(&op, sizeof op);
+        mix(&n, sizeof n);
+        mix(&w->p, sizeof w->p);
+        mix(&sched_used, sizeof sched_used);
+        mix(&w->arity, sizeof w->arity);
+        mix(&bc, sizeof bc);
+        mix(&c.lr, sizeof c.lr);
+        mix(&c.mu, sizeof c.mu);
+        mix(&c.wd, sizeof c.wd);
+        mix(&c.inv_b, sizeof c.inv_b);
+        c.sig = h;
+    }
     c.op = op;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;

@@ -11,7 +11,8 @@
 #define FC_BAR_SLOTS 2           // 0 = entry barrier, 1 = exit barrier
 
 // Layout of the flag area at the start of every rank's heap (uint32 words):
-//   bar[FC_BAR_SLOTS][FC_MAX_CTAS][FC_MAX_RANKS]   per-CTA all-to-all barriers
+//   bar[FC_BAR_SLOTS][FC_MAX_CTAS][FC_MAX_RANKS]   per-CTA all-to-all barriers, uint64 each:
+//                                                  epoch | call signature << 32 (2 words)
 //   red[FC_MAX_LEVELS][max_chunks]                 "partial of chunk c for level l+1 ready"
 //   av[max_chunks]                                 "broadcast value of chunk c has arrived"
 // All flags hold the epoch of the call that last wrote them (monotonic, never reset).
@@ -25,7 +26,7 @@ struct FcFlagLayout {
 static inline FcFlagLayout fc_flag_layout(int64_t heap_bytes) {
     FcFlagLayout L;
     L.max_chunks = heap_bytes / (4 * (int64_t)FC_CHUNK_FLOATS) + 1;
-    L.bar_words = (int64_t)FC_BAR_SLOTS * FC_MAX_CTAS * FC_MAX_RANKS;
+    L.bar_words = 2 * (int64_t)FC_BAR_SLOTS * FC_MAX_CTAS * FC_MAX_RANKS;
     L.red_words = L.bar_words + (int64_t)FC_MAX_LEVELS * L.max_chunks;
     int64_t words = L.red_words + L.max_chunks;
     int64_t bytes = words * 4;
@@ -43,6 +44,7 @@ struct FcColl {
     int rank;          // >= 0: this process's rank; -1: virtual world, rank = blockIdx.y
     int p;             // world size
     uint32_t epoch;    // call counter (same on every rank)
+    uint32_t sig;      // hash of (op, n, schedule, hyper-parameters): must match on every rank
     int op;            // FcOp
     uint64_t timeout_ns;
     int* status;       // sticky device status (FC_OK until a timeout)

@@ -34,7 +34,8 @@ constexpr int TREE_T = 256;                       // threads per CTA (tree sched
 constexpr int FLAT_T = 512;                       // threads per CTA (FLAT / PS), one CTA per SM
 // float4 per thread per operand in flight in FLAT: enough remote bytes in flight
 // (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
-#define FLAT_UNROLL(P) ((P) <= 3 ? 2 : 1)
+// (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*)
+#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : 2)
 constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
 constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
 static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
@@ -46,9 +47,10 @@ __device__ __forceinline__ int my_rank(const FcColl& c) {
 __device__ __forceinline__ uint32_t* flag_base(const FcColl& c, int q) {
     return reinterpret_cast<uint32_t*>(c.peers.heap[q]);
 }
-__device__ __forceinline__ uint32_t* bar_flag(const FcColl& c, int owner, int slot, int cta,
+__device__ __forceinline__ uint64_t* bar_flag(const FcColl& c, int owner, int slot, int cta,
                                               int src) {
-    return flag_base(c, owner) + ((int64_t)(slot * FC_MAX_CTAS + cta) * FC_MAX_RANKS + src);
+    return reinterpret_cast<uint64_t*>(flag_base(c, owner)) +
+           ((int64_t)(slot * FC_MAX_CTAS + cta) * FC_MAX_RANKS + src);
 }
 __device__ __forceinline__ uint32_t* red_flag(const FcColl& c, int owner, int l, int64_t cc) {
     return flag_base(c, owner) + c.bar_words + (int64_t)l * c.max_chunks + cc;
@@ -81,15 +83,44 @@ __device__ __forceinline__ void trace(const FcColl& c, int slot) {
 //  exit (slot 1): st.release.sys orders the CTA's earlier writes — peer stores
 //    included; the __syncthreads orders the other threads' writes before it
 //    (PTX causality through bar.sync) — ahead of the stamp.
+// A stamp is one 64-bit word: epoch | signature << 32.  The signature hashes the
+// call's op, n, executor and hyper-parameters; a peer whose signature differs
+// made a different call (MPI/NCCL rule broken) -> sticky FC_ERR_MISMATCH on
+// every rank and no data is touched.
 __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
     __syncthreads();
     const int t = threadIdx.x;
     bool good = true;
     if (t < c.p && t != rank) {
-        uint32_t* dst = bar_flag(c, t, slot, blockIdx.x, rank);
-        if (slot == 0) st_relaxed_sys(dst, c.epoch);
-        else st_release_sys(dst, c.epoch);
-        good = wait_flag(bar_flag(c, rank, slot, blockIdx.x, t), c.epoch, c.timeout_ns, c.status);
+        const uint64_t stamp = (uint64_t)c.epoch | ((uint64_t)c.sig << 32);
+        uint64_t* dst = bar_flag(c, t, slot, blockIdx.x, rank);
+        if (slot == 0) st_relaxed_sys64(dst, stamp);
+        else st_release_sys64(dst, stamp);
+        const uint64_t* f = bar_flag(c, rank, slot, blockIdx.x, t);
+        uint64_t v = ld_acquire_sys64(f);
+        if (!reached((uint32_t)v, c.epoch)) {
+            const uint64_t t0 = globaltimer();
+            uint32_t spins = 0;
+            while (true) {
+                v = ld_relaxed_sys64(f);
+                if (reached((uint32_t)v, c.epoch)) {
+                    v = ld_acquire_sys64(f);
+                    break;
+                }
+                if ((++spins & 63u) == 0) {
+                    if (*(volatile int*)c.status != FC_OK) { good = false; break; }
+                    if (globaltimer() - t0 > c.timeout_ns) {
+                        atomicCAS(c.status, FC_OK, FC_ERR_TIMEOUT);
+                        good = false;
+                        break;
+                    }
+                }
+            }
+        }
+        if (good && (uint32_t)v == c.epoch && (uint32_t)(v >> 32) != c.sig) {
+            atomicCAS(c.status, FC_OK, FC_ERR_MISMATCH);
+            good = false;
+        }
     }
     return __syncthreads_and(good) != 0;
 }
@@ -469,11 +500,8 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
 }
 
 // ------------------------------------------------------------ dispatch -----
-template <int P>
-static const void* flat_for(int K) {
-    // K >= P is the same association as K = P (one level, sequential)
-    if (K >= P) K = P;
-    constexpr int U = FLAT_UNROLL(P);
+template <int P, int U>
+static const void* flat_for_u(int K) {
     switch (K) {
         case 2: return (const void*)flat_kernel<P, 2, U>;
 #define FC_K(k) case k: if constexpr (P >= k) return (const void*)flat_kernel<P, k, U>; else return nullptr;
@@ -481,6 +509,28 @@ static const void* flat_for(int K) {
 #undef FC_K
     }
     return nullptr;
+}
+
+// Unroll override for tuning experiments (FC_FLAT_UNROLL=1|2|4; 0 = default).
+static int flat_unroll_override() {
+    static int u = -1;
+    if (u < 0) {
+        const char* e = getenv("FC_FLAT_UNROLL");
+        u = e ? atoi(e) : 0;
+    }
+    return u;
+}
+
+template <int P>
+static const void* flat_for(int K) {
+    // K >= P is the same association as K = P (one level, sequential)
+    if (K >= P) K = P;
+    switch (flat_unroll_override()) {
+        case 1: return flat_for_u<P, 1>(K);
+        case 2: return flat_for_u<P, 2>(K);
+        case 4: return flat_for_u<P, 4>(K);
+        default: return flat_for_u<P, FLAT_UNROLL(P)>(K);
+    }
 }
 
 template <int P>

@@ -84,6 +84,20 @@ def main():
     dist.all_reduce(hi, op=dist.ReduceOp.MAX)
     if lo.item() != hi.item():
         fails.append("digest differs across ranks")
+    # mismatch test (fresh world): ranks disagree on n -> every rank reports
+    # FC_ERR_MISMATCH and no data is touched
+    W2 = fc.World.create(heap_bytes_for(4096 + 4096), timeout_s=5.0)
+    g2 = W2.alloc(2048)
+    g2.fill_(float(rank + 1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    fc.firecaffe_tree_allreduce(g2, W2, n=1000 + 4 * rank)
+    st2 = W2.poll()
+    if st2 != 3:
+        fails.append(f"expected FC_ERR_MISMATCH, got {st2}")
+    if not bool((g2 == float(rank + 1)).all().item()):
+        fails.append("mismatched call modified data")
+    dist.barrier()
     nf = torch.tensor([len(fails)], device=dev)
     dist.all_reduce(nf)
     if fails:
