@@ -84,6 +84,27 @@ def grads(n: int, p: int, seed: int = SEED, device="cpu", dist: str = "paper") -
     return torch.stack([grad(n, r, seed, device, dist) for r in range(p)]) if p else torch.empty(0, n)
 
 
+def caffe_blobs(n: int, n_layers: int = 12, seed: int = SEED):
+    """A Caffe-like blob table over a flat vector of n params: per layer one
+    weight blob (lr_mult 1, decay_mult 1) followed by one bias blob (lr_mult 2,
+    decay_mult 0), bias sizes ragged (not multiples of 4).  Returns
+    (begins, lr_mults, decay_mults).  For n < 4·n_layers: a single blob."""
+    if n < 4 * n_layers:
+        return [0], [1.0], [1.0]
+    g = _gen("cpu", seed + 17)
+    share = torch.rand(n_layers, generator=g, dtype=torch.float64) + 0.2
+    sizes = (share / share.sum() * n).floor().to(torch.int64).tolist()
+    sizes[-1] += n - sum(sizes)
+    begins, lrm, dm, pos = [], [], [], 0
+    for s in sizes:
+        nb = max(1, min(s // 2, 3 + int(torch.randint(0, 1000, (1,), generator=g))))  # ragged bias
+        begins += [pos, pos + s - nb]
+        lrm += [1.0, 2.0]
+        dm += [1.0, 0.0]
+        pos += s
+    return begins, lrm, dm
+
+
 def weights(n: int, seed: int = SEED, device="cpu") -> torch.Tensor:
     """Replicated initial weights, N(0, 0.01²)."""
     return torch.randn(n, generator=_gen(device, seed + 11), device=device, dtype=torch.float32) * 0.01

@@ -193,6 +193,55 @@ fc_status firecaffe_tree_allreduce_sgd(float* w, float* grad, float* mom, int64_
  * holds it on return.  Equal bitwise to firecaffe_tree_allreduce with arity p. */
 fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* world, void* stream);
 
+/* ------------------------------------------------ Caffe per-blob multipliers
+ * The flat parameter vector is a concatenation of blobs (layers' weights and
+ * biases).  Caffe gives each blob an lr_mult and a decay_mult (settings
+ * "consistent with the Caffe configuration files"; typical: biases lr_mult 2,
+ * decay_mult 0).  Blob s covers [segs[s].begin, segs[s+1].begin) (the last up to
+ * n); per element the update uses local_lr = fl(lr*lr_mult), local_wd =
+ * fl(wd*decay_mult) in the firecaffe_sgd_step rule (R20).  All
+ * multipliers 1 gives exactly firecaffe_sgd_step's bits.
+ * firecaffe_segments_create validates the HOST table (segs[0].begin == 0,
+ * strictly increasing, every begin < n, finite multipliers >= 0) and copies it
+ * to the current device once; the handle is then passed to the *_segments
+ * calls, whose n must equal the table's n.  1 <= nseg <= 65536. */
+typedef struct {
+    int64_t begin;
+    float lr_mult;
+    float decay_mult;
+} fc_segment;
+typedef struct fc_segments fc_segments;
+fc_status firecaffe_segments_create(const fc_segment* segs, int nseg, int64_t n, fc_segments** out);
+fc_status firecaffe_segments_destroy(fc_segments* segs);
+fc_status firecaffe_sgd_step_segments(float* w, const float* grad, float* mom, int64_t n, float lr,
+                                      float mu, float wd, int64_t batch, const fc_segments* segs,
+                                      void* stream);
+fc_status firecaffe_tree_allreduce_sgd_segments(float* w, float* grad, float* mom, int64_t n,
+                                                float lr, float mu, float wd, int64_t batch,
+                                                const fc_segments* segs, fc_world* world,
+                                                void* stream);
+
+/* ------------------------------------------------ learning-rate schedules
+ * The paper's schedules (R21): FIXED; STEP gamma^floor(iter/stepsize);
+ * MULTISTEP gamma^#{steps[k] <= iter} ("reduce this by a factor of 10x twice",
+ * P:407); POLY (1 - iter/max_iter)^power (power 0.5).  Evaluated in
+ * double and rounded once to fp32; host-only.  Returns -1 for invalid input
+ * (iter < 0, base_lr <= 0, stepsize < 1 for STEP, iter > max_iter for POLY,
+ * nsteps outside 0..FC_LR_MAX_STEPS). */
+typedef enum { FC_LR_FIXED = 0, FC_LR_STEP = 1, FC_LR_MULTISTEP = 2, FC_LR_POLY = 3 } fc_lr_policy;
+#define FC_LR_MAX_STEPS 16
+typedef struct {
+    int policy;       /* fc_lr_policy */
+    float base_lr;
+    float gamma;
+    int64_t stepsize;
+    float power;
+    int64_t max_iter;
+    int nsteps;
+    int64_t steps[FC_LR_MAX_STEPS];
+} fc_lr_schedule;
+float firecaffe_lr_at(const fc_lr_schedule* sched, int64_t iter);
+
 /* Linear learning-rate scaling with the batch size:
  * returns fl(base_lr * batch / base_batch) computed in double, e.g. (0.01, 256, 1024) -> 0.04.
  * Returns 0 for base_batch < 1 or batch < 1. */

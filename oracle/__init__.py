@@ -59,8 +59,11 @@ def lib():
         L.oracle_abs_sum_f64.argtypes = [P, I, I64, P]
         L.oracle_sgd_f64.argtypes = [P, P, P, I64, F, F, F, I64]
         L.oracle_tree_plan.argtypes = [I, I, P, I]
+        L.oracle_sgd_segments.argtypes = [P, P, P, I64, F, F, F, I64, P, P, P, I]
+        L.oracle_lr_at.argtypes = [I, F, I64, F, I64, P, I, F, I64]
+        L.oracle_lr_at.restype = F
         for f in ("oracle_tree_sum", "oracle_ps_sum", "oracle_sgd", "oracle_sum_f64",
-                  "oracle_abs_sum_f64", "oracle_sgd_f64", "oracle_tree_plan"):
+                  "oracle_abs_sum_f64", "oracle_sgd_f64", "oracle_tree_plan", "oracle_sgd_segments"):
             getattr(L, f).restype = I
         _lib = L
     return _lib
@@ -107,6 +110,35 @@ def sgd(w, v, S, lr: float, mu: float, wd: float, batch: int):
     assert v.shape == (n,) and S.shape == (n,)
     _check(lib().oracle_sgd(_ptr(w), _ptr(v), _ptr(S), n, lr, mu, wd, batch), "sgd")
     return w, v
+
+
+def sgd_segments(w, v, S, lr: float, mu: float, wd: float, batch: int, begins, lr_mults, decay_mults):
+    """SGD with Caffe per-blob lr_mult / decay_mult (reading R20)."""
+    w = _f32(w).copy()
+    v = _f32(v).copy()
+    S = _f32(S)
+    n = w.shape[0]
+    b = np.ascontiguousarray(begins, np.int64)
+    lm = np.ascontiguousarray(lr_mults, np.float32)
+    dm = np.ascontiguousarray(decay_mults, np.float32)
+    assert b.shape == lm.shape == dm.shape
+    _check(lib().oracle_sgd_segments(_ptr(w), _ptr(v), _ptr(S), n, lr, mu, wd, batch, _ptr(b), _ptr(lm), _ptr(dm),
+                                     b.shape[0]), "sgd_segments")
+    return w, v
+
+
+POLICY = {"fixed": 0, "step": 1, "multistep": 2, "poly": 3}
+
+
+def lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, stepsize: int = 0, steps=(),
+          power: float = 0.5, max_iter: int = 0) -> float:
+    """Learning rate at iteration `it` (P:407 step, P:451-452 poly; reading R21)."""
+    st = np.ascontiguousarray(steps, np.int64)
+    r = lib().oracle_lr_at(POLICY[policy], base_lr, int(it), gamma, int(stepsize),
+                           _ptr(st) if st.size else None, int(st.size), power, int(max_iter))
+    if r < 0:
+        raise ValueError("lr_at: invalid arguments")
+    return float(np.float32(r))
 
 
 def sum_f64(g) -> np.ndarray:

@@ -127,6 +127,75 @@ int oracle_sgd(float* w, float* v, const float* S, int64_t n, float lr, float mu
 }
 
 // ---------------------------------------------------------------------------
+// SGD with Caffe per-blob multipliers ("consistent with
+// the Caffe configuration files", P:357-358 per-layer settings).  The flat
+// parameter vector is a concatenation of blobs; blob s covers
+// [begin[s], begin[s+1]) (the last one up to n) and carries lr_mult[s],
+// decay_mult[s] (Caffe ParamSpec).  Per element (reading R20):
+//   local_lr = fl(lr · lr_mult),  local_wd = fl(wd · decay_mult)
+//   then the oracle_sgd rule with (local_lr, local_wd).
+// With every multiplier 1 this is bit-identical to oracle_sgd.
+// ---------------------------------------------------------------------------
+int oracle_sgd_segments(float* w, float* v, const float* S, int64_t n, float lr, float mu,
+                        float wd, int64_t batch, const int64_t* begin, const float* lr_mult,
+                        const float* decay_mult, int nseg) {
+    if (n < 0 || batch < 1 || nseg < 1 || !begin || !lr_mult || !decay_mult) return 1;
+    if (n > 0 && (!w || !v || !S)) return 1;
+    if (begin[0] != 0) return 1;
+    for (int s = 1; s < nseg; ++s)
+        if (begin[s] <= begin[s - 1] || begin[s] >= n) return 1;
+    const float inv_b = 1.0f / (float)batch;
+    int s = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        while (s + 1 < nseg && begin[s + 1] <= i) ++s;  // blob containing element i
+        const float local_lr = lr * lr_mult[s];
+        const float local_wd = wd * decay_mult[s];
+        const float g = S[i] * inv_b;
+        const float d = std::fma(local_wd, w[i], g);
+        const float t = local_lr * d;
+        const float vn = std::fma(mu, v[i], t);
+        const float wn = w[i] - vn;
+        v[i] = vn;
+        w[i] = wn;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Learning-rate schedules of the paper:
+//   policy 0 fixed      : base_lr
+//   policy 1 step       : base_lr · gamma^floor(iter / stepsize)
+//   policy 2 multistep  : base_lr · gamma^#{k : steps[k] <= iter}   ("reduce this by
+//                          a factor of 10x twice")
+//   policy 3 poly       : base_lr · (1 − iter/max_iter)^power      (power 0.5)
+// Evaluated in double, rounded once to fp32 (reading R21).  Returns -1 on
+// invalid arguments (iter < 0, poly with iter > max_iter, stepsize < 1, ...).
+// ---------------------------------------------------------------------------
+float oracle_lr_at(int policy, float base_lr, int64_t iter, float gamma, int64_t stepsize,
+                   const int64_t* steps, int nsteps, float power, int64_t max_iter) {
+    if (iter < 0 || !(base_lr > 0.0f)) return -1.0f;
+    double f = 1.0;
+    if (policy == 0) {
+        f = 1.0;
+    } else if (policy == 1) {
+        if (stepsize < 1) return -1.0f;
+        f = std::pow((double)gamma, (double)(iter / stepsize));
+    } else if (policy == 2) {
+        if (nsteps < 0 || (nsteps > 0 && !steps)) return -1.0f;
+        int k = 0;
+        for (int j = 0; j < nsteps; ++j)
+            if (steps[j] <= iter) ++k;
+        f = std::pow((double)gamma, (double)k);
+    } else if (policy == 3) {
+        if (max_iter < 1 || iter > max_iter) return -1.0f;
+        f = std::pow(1.0 - (double)iter / (double)max_iter, (double)power);
+    } else {
+        return -1.0f;
+    }
+    return (float)((double)base_lr * f);
+}
+
+// ---------------------------------------------------------------------------
 // float64 references (north_star: "within 1e-6 relative error (fp32) against
 // a naive left-to-right float64 sum").
 // ---------------------------------------------------------------------------

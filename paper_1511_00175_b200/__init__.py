@@ -100,3 +100,61 @@ def firecaffe_plan_owned_range(world_size: int, sched: int, rank: int, n: int):
 
 def firecaffe_tune_sgd_unroll(u: int):
     load().firecaffe_tune_sgd_unroll(int(u))
+
+
+class Segments:
+    """Caffe per-blob lr_mult / decay_mult table (header: fc_segments), uploaded once
+    to the current device.  `begins[s]` is blob s's first element."""
+
+    def __init__(self, begins, lr_mults, decay_mults, n: int):
+        if not (len(begins) == len(lr_mults) == len(decay_mults)):
+            raise ValueError("begins, lr_mults, decay_mults must have equal length")
+        arr = (_lib.FcSegment * len(begins))(*[_lib.FcSegment(int(b), float(l), float(d))
+                                               for b, l, d in zip(begins, lr_mults, decay_mults)])
+        h = ctypes.c_void_p()
+        check(load().firecaffe_segments_create(arr, len(begins), int(n), ctypes.byref(h)),
+              "firecaffe_segments_create")
+        self.handle = h.value
+        self.n = int(n)
+
+    def close(self):
+        if self.handle:
+            load().firecaffe_segments_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def firecaffe_sgd_step_segments(w, grad, mom, lr, mu, wd, batch, segs: Segments, n=None, stream=None):
+    """firecaffe_sgd_step with Caffe per-blob multipliers."""
+    check(load().firecaffe_sgd_step_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd, int(batch),
+                                             segs.handle, _stream(stream)), "firecaffe_sgd_step_segments")
+
+
+def firecaffe_tree_allreduce_sgd_segments(w, grad, mom, lr, mu, wd, batch, segs: Segments, world: "World",
+                                          n=None, stream=None):
+    """firecaffe_tree_allreduce_sgd with Caffe per-blob multipliers."""
+    check(load().firecaffe_tree_allreduce_sgd_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd,
+                                                       int(batch), segs.handle, world.handle, _stream(stream)),
+          "firecaffe_tree_allreduce_sgd_segments")
+
+
+def firecaffe_lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, stepsize: int = 0, steps=(),
+                    power: float = 0.5, max_iter: int = 0) -> float:
+    """Learning rate of the paper's schedules at iteration `it` (header: firecaffe_lr_at)."""
+    s = _lib.FcLrSchedule()
+    s.policy = _lib.LR_POLICY[policy]
+    s.base_lr, s.gamma, s.stepsize, s.power, s.max_iter = base_lr, gamma, int(stepsize), power, int(max_iter)
+    if len(steps) > _lib.FC_LR_MAX_STEPS:
+        raise ValueError("too many steps")
+    s.nsteps = len(steps)
+    for i, v in enumerate(steps):
+        s.steps[i] = int(v)
+    r = load().firecaffe_lr_at(ctypes.byref(s), int(it))
+    if r < 0:
+        raise ValueError("firecaffe_lr_at: invalid schedule or iteration")
+    return r

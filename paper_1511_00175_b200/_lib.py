@@ -57,7 +57,26 @@ SIGNATURES = {
     "firecaffe_world_set_trace": (_I, [_P, _P, _I64]),
     "firecaffe_world_last_grid": (_I, [_P]),
     "firecaffe_version": (ctypes.c_char_p, []),
+    "firecaffe_segments_create": (_I, [_P, _I, _I64, _PP]),
+    "firecaffe_segments_destroy": (_I, [_P]),
+    "firecaffe_sgd_step_segments": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
+    "firecaffe_tree_allreduce_sgd_segments": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
+    "firecaffe_lr_at": (_F, [_P, _I64]),
 }
+
+FC_LR_MAX_STEPS = 16
+LR_POLICY = {"fixed": 0, "step": 1, "multistep": 2, "poly": 3}
+
+
+class FcSegment(ctypes.Structure):
+    """fc_segment: one Caffe blob of the flat parameter vector."""
+    _fields_ = [("begin", ctypes.c_int64), ("lr_mult", ctypes.c_float), ("decay_mult", ctypes.c_float)]
+
+
+class FcLrSchedule(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int), ("base_lr", ctypes.c_float), ("gamma", ctypes.c_float),
+                ("stepsize", ctypes.c_int64), ("power", ctypes.c_float), ("max_iter", ctypes.c_int64),
+                ("nsteps", ctypes.c_int), ("steps", ctypes.c_int64 * FC_LR_MAX_STEPS)]
 
 _lib = None
 

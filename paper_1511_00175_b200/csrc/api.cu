@@ -12,6 +12,16 @@
 
 #define FC_VERSION_STR "firecaffe-b200 0.1.0 sm_100a"
 
+struct fc_segments {
+    int nseg;
+    int64_t n;
+    int device;
+    uint32_t hash;  // of the host table: part of the collective call signature
+    int64_t* d_begin;
+    float* d_lrm;
+    float* d_dm;
+};
+
 struct fc_world {
     int rank;  // -1 for a virtual world
     int p;
@@ -292,17 +302,52 @@ fc_status firecaffe_owned_range(const fc_world* w, int rank, int64_t n, int64_t*
     return firecaffe_plan_owned_range(w->p, w->sched, rank, n, begin, end);
 }
 
+static fc_status sgd_impl(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
+                          float wd, int64_t batch, const fc_segments* segs, void* stream);
+
 fc_status firecaffe_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr,
                              float mu, float wd, int64_t batch, void* stream) {
+    return sgd_impl(w, grad, mom, n, lr, mu, wd, batch, nullptr, stream);
+}
+
+fc_status firecaffe_sgd_step_segments(float* w, const float* grad, float* mom, int64_t n, float lr,
+                                      float mu, float wd, int64_t batch, const fc_segments* segs,
+                                      void* stream) {
+    if (!segs) return FC_ERR_INVALID_ARG;
+    return sgd_impl(w, grad, mom, n, lr, mu, wd, batch, segs, stream);
+}
+
+static fc_status check_segs(const fc_segments* segs, int64_t n, FcSegs* out) {
+    out->begin = nullptr;
+    out->lrm = nullptr;
+    out->dm = nullptr;
+    out->nseg = 0;
+    if (!segs) return FC_OK;
+    if (segs->n != n) return FC_ERR_INVALID_ARG;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
+    if (cur != segs->device) return FC_ERR_MISMATCH;
+    out->begin = segs->d_begin;
+    out->lrm = segs->d_lrm;
+    out->dm = segs->d_dm;
+    out->nseg = segs->nseg;
+    return FC_OK;
+}
+
+static fc_status sgd_impl(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
+                          float wd, int64_t batch, const fc_segments* segs, void* stream) {
     if (n < 0) return FC_ERR_INVALID_ARG;
     fc_status st = check_hyper(lr, mu, wd, batch);
     if (st != FC_OK) return st;
-    if (n == 0) return FC_OK;
+    if (n == 0) return segs && segs->n != 0 ? FC_ERR_INVALID_ARG : FC_OK;
     if (check_vec(w, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
     const int64_t bytes = n * 4;
     if (overlap(w, grad, bytes) || overlap(w, mom, bytes) || overlap(grad, mom, bytes))
         return FC_ERR_INVALID_ARG;
-    cudaError_t e = launch_sgd_step(w, grad, mom, n, lr, mu, wd, inv_batch(batch),
+    FcSegs sd;
+    st = check_segs(segs, n, &sd);
+    if (st != FC_OK) return st;
+    cudaError_t e = launch_sgd_step(w, grad, mom, n, lr, mu, wd, inv_batch(batch), sd,
                                     (cudaStream_t)stream);
     return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
@@ -317,7 +362,8 @@ static int64_t heap_offset(const fc_world* w, const void* p, int64_t n) {
 }
 
 static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* mom, int64_t n,
-                            float lr, float mu, float wd, int64_t batch, void* stream) {
+                            float lr, float mu, float wd, int64_t batch,
+                            const fc_segments* segs, void* stream) {
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
     if (cur != w->device) return FC_ERR_MISMATCH;
@@ -327,6 +373,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     if (c.off_grad < 0) return FC_ERR_NOT_SYMMETRIC;
     c.off_w = 0;
     c.off_mom = -1;
+    uint32_t seg_hash = 0;
     if (op == FC_OP_ALLREDUCE_SGD) {
         c.off_w = heap_offset(w, wt, n);
         if (c.off_w < 0) return FC_ERR_NOT_SYMMETRIC;
@@ -339,6 +386,9 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         c.mu = mu;
         c.wd = wd;
         c.inv_b = inv_batch(batch);
+        fc_status st = check_segs(segs, n, &c.segs);
+        if (st != FC_OK) return st;
+        if (segs) seg_hash = segs->hash;
     }
     for (int q = 0; q < w->p; ++q) c.peers.heap[q] = w->peer[q];
     c.rank = w->virt ? -1 : w->rank;
@@ -362,6 +412,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         mix(&c.mu, sizeof c.mu);
         mix(&c.wd, sizeof c.wd);
         mix(&c.inv_b, sizeof c.inv_b);
+        mix(&seg_hash, sizeof seg_hash);
         c.sig = h;
     }
     c.op = op;
@@ -391,29 +442,132 @@ fc_status firecaffe_tree_allreduce(float* grad, int64_t n, fc_world* w, void* st
     if (!w || n < 0) return FC_ERR_INVALID_ARG;
     if (n == 0 || w->p == 1) return FC_OK;
     if (check_vec(grad, n)) return FC_ERR_INVALID_ARG;
-    return collective(w, FC_OP_ALLREDUCE, nullptr, grad, nullptr, n, 0, 0, 0, 1, stream);
+    return collective(w, FC_OP_ALLREDUCE, nullptr, grad, nullptr, n, 0, 0, 0, 1, nullptr, stream);
 }
 
 fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* w, void* stream) {
     if (!w || n < 0) return FC_ERR_INVALID_ARG;
     if (n == 0 || w->p == 1) return FC_OK;
     if (check_vec(grad, n)) return FC_ERR_INVALID_ARG;
-    return collective(w, FC_OP_PS, nullptr, grad, nullptr, n, 0, 0, 0, 1, stream);
+    return collective(w, FC_OP_PS, nullptr, grad, nullptr, n, 0, 0, 0, 1, nullptr, stream);
+}
+
+static fc_status fused_impl(float* wt, float* grad, float* mom, int64_t n, float lr, float mu,
+                            float wd, int64_t batch, const fc_segments* segs, fc_world* w,
+                            void* stream) {
+    if (!w || n < 0) return FC_ERR_INVALID_ARG;
+    fc_status st = check_hyper(lr, mu, wd, batch);
+    if (st != FC_OK) return st;
+    if (n == 0) return segs && segs->n != 0 ? FC_ERR_INVALID_ARG : FC_OK;
+    if (check_vec(wt, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    const int64_t bytes = n * 4;
+    if (overlap(wt, grad, bytes) || overlap(wt, mom, bytes) || overlap(grad, mom, bytes))
+        return FC_ERR_INVALID_ARG;
+    if (w->p == 1) return sgd_impl(wt, grad, mom, n, lr, mu, wd, batch, segs, stream);
+    return collective(w, FC_OP_ALLREDUCE_SGD, wt, grad, mom, n, lr, mu, wd, batch, segs, stream);
 }
 
 fc_status firecaffe_tree_allreduce_sgd(float* wt, float* grad, float* mom, int64_t n, float lr,
                                        float mu, float wd, int64_t batch, fc_world* w,
                                        void* stream) {
-    if (!w || n < 0) return FC_ERR_INVALID_ARG;
-    fc_status st = check_hyper(lr, mu, wd, batch);
-    if (st != FC_OK) return st;
-    if (n == 0) return FC_OK;
-    if (check_vec(wt, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
-    const int64_t bytes = n * 4;
-    if (overlap(wt, grad, bytes) || overlap(wt, mom, bytes) || overlap(grad, mom, bytes))
-        return FC_ERR_INVALID_ARG;
-    if (w->p == 1) return firecaffe_sgd_step(wt, grad, mom, n, lr, mu, wd, batch, stream);
-    return collective(w, FC_OP_ALLREDUCE_SGD, wt, grad, mom, n, lr, mu, wd, batch, stream);
+    return fused_impl(wt, grad, mom, n, lr, mu, wd, batch, nullptr, w, stream);
+}
+
+fc_status firecaffe_tree_allreduce_sgd_segments(float* wt, float* grad, float* mom, int64_t n,
+                                                float lr, float mu, float wd, int64_t batch,
+                                                const fc_segments* segs, fc_world* w,
+                                                void* stream) {
+    if (!segs) return FC_ERR_INVALID_ARG;
+    return fused_impl(wt, grad, mom, n, lr, mu, wd, batch, segs, w, stream);
+}
+
+fc_status firecaffe_segments_create(const fc_segment* segs, int nseg, int64_t n,
+                                    fc_segments** out) {
+    if (!out) return FC_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!segs || nseg < 1 || nseg > 65536 || n < 1) return FC_ERR_INVALID_ARG;
+    if (segs[0].begin != 0) return FC_ERR_INVALID_ARG;
+    for (int s = 0; s < nseg; ++s) {
+        if (s > 0 && segs[s].begin <= segs[s - 1].begin) return FC_ERR_INVALID_ARG;
+        if (segs[s].begin >= n) return FC_ERR_INVALID_ARG;
+        if (!(segs[s].lr_mult >= 0.0f) || !std::isfinite(segs[s].lr_mult)) return FC_ERR_INVALID_ARG;
+        if (!(segs[s].decay_mult >= 0.0f) || !std::isfinite(segs[s].decay_mult))
+            return FC_ERR_INVALID_ARG;
+    }
+    fc_segments* t = new fc_segments();
+    memset(t, 0, sizeof(*t));
+    t->nseg = nseg;
+    t->n = n;
+    if (cudaGetDevice(&t->device) != cudaSuccess) {
+        delete t;
+        return FC_ERR_CUDA;
+    }
+    int64_t* hb = new int64_t[nseg];
+    float* hl = new float[nseg];
+    float* hd = new float[nseg];
+    uint32_t h = 2166136261u;
+    for (int s = 0; s < nseg; ++s) {
+        hb[s] = segs[s].begin;
+        hl[s] = segs[s].lr_mult;
+        hd[s] = segs[s].decay_mult;
+        const unsigned char* b = (const unsigned char*)&segs[s];
+        for (size_t i = 0; i < sizeof(fc_segment); ++i) h = (h ^ b[i]) * 16777619u;
+    }
+    t->hash = h;
+    bool ok = cudaMalloc(&t->d_begin, nseg * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&t->d_lrm, nseg * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&t->d_dm, nseg * sizeof(float)) == cudaSuccess &&
+              cudaMemcpy(t->d_begin, hb, nseg * sizeof(int64_t), cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(t->d_lrm, hl, nseg * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(t->d_dm, hd, nseg * sizeof(float), cudaMemcpyHostToDevice) == cudaSuccess;
+    delete[] hb;
+    delete[] hl;
+    delete[] hd;
+    if (!ok) {
+        firecaffe_segments_destroy(t);
+        return FC_ERR_CUDA;
+    }
+    *out = t;
+    return FC_OK;
+}
+
+fc_status firecaffe_segments_destroy(fc_segments* t) {
+    if (!t) return FC_OK;
+    if (t->d_begin) cudaFree(t->d_begin);
+    if (t->d_lrm) cudaFree(t->d_lrm);
+    if (t->d_dm) cudaFree(t->d_dm);
+    delete t;
+    return FC_OK;
+}
+
+// The paper's learning-rate schedules, in double, one
+// rounding to fp32 (R21).
+float firecaffe_lr_at(const fc_lr_schedule* s, int64_t iter) {
+    if (!s || iter < 0 || !(s->base_lr > 0.0f)) return -1.0f;
+    double f;
+    switch (s->policy) {
+        case FC_LR_FIXED:
+            f = 1.0;
+            break;
+        case FC_LR_STEP:
+            if (s->stepsize < 1) return -1.0f;
+            f = std::pow((double)s->gamma, (double)(iter / s->stepsize));
+            break;
+        case FC_LR_MULTISTEP: {
+            if (s->nsteps < 0 || s->nsteps > FC_LR_MAX_STEPS) return -1.0f;
+            int k = 0;
+            for (int j = 0; j < s->nsteps; ++j) k += s->steps[j] <= iter;
+            f = std::pow((double)s->gamma, (double)k);
+            break;
+        }
+        case FC_LR_POLY:
+            if (s->max_iter < 1 || iter > s->max_iter) return -1.0f;
+            f = std::pow(1.0 - (double)iter / (double)s->max_iter, (double)s->power);
+            break;
+        default:
+            return -1.0f;
+    }
+    return (float)((double)s->base_lr * f);
 }
 
 void firecaffe_tune_sgd_unroll(int u) { set_sgd_unroll(u); }

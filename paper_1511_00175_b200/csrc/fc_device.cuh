@@ -152,6 +152,47 @@ __device__ __forceinline__ void sgd4(const float4& S, float4& w, float4& v, floa
     sgd1(S.w, w.w, v.w, lr, mu, wd, inv_b);
 }
 
+// ---- Caffe per-blob multipliers (R20) ---------------------------
+// Blob containing element e: largest k with begin[k] <= e (begin[0] == 0).
+__device__ __forceinline__ int seg_find(const FcSegs& s, int64_t e) {
+    int lo = 0, hi = s.nseg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(s.begin + mid) <= e) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__device__ __forceinline__ void sgd1_seg(const FcSegs& s, int64_t e, float S, float& w, float& v,
+                                         float lr, float mu, float wd, float inv_b) {
+    const int k = seg_find(s, e);
+    sgd1(S, w, v, __fmul_rn(lr, __ldg(s.lrm + k)), mu, __fmul_rn(wd, __ldg(s.dm + k)), inv_b);
+}
+// Four consecutive elements e..e+3; one lookup unless a blob boundary falls inside.
+__device__ __forceinline__ void sgd4_seg(const FcSegs& s, int64_t e, const float4& S, float4& w,
+                                         float4& v, float lr, float mu, float wd, float inv_b) {
+    const int k = seg_find(s, e);
+    const bool whole = (k + 1 >= s.nseg) || (__ldg(s.begin + k + 1) > e + 3);
+    if (whole) {
+        sgd4(S, w, v, __fmul_rn(lr, __ldg(s.lrm + k)), mu, __fmul_rn(wd, __ldg(s.dm + k)), inv_b);
+    } else {
+        sgd1_seg(s, e + 0, S.x, w.x, v.x, lr, mu, wd, inv_b);
+        sgd1_seg(s, e + 1, S.y, w.y, v.y, lr, mu, wd, inv_b);
+        sgd1_seg(s, e + 2, S.z, w.z, v.z, lr, mu, wd, inv_b);
+        sgd1_seg(s, e + 3, S.w, w.w, v.w, lr, mu, wd, inv_b);
+    }
+}
+// Dispatch: uniform fast path when no table is given.
+__device__ __forceinline__ void sgd4_any(const FcSegs& s, int64_t e, const float4& S, float4& w,
+                                         float4& v, float lr, float mu, float wd, float inv_b) {
+    if (s.nseg > 0) sgd4_seg(s, e, S, w, v, lr, mu, wd, inv_b);
+    else sgd4(S, w, v, lr, mu, wd, inv_b);
+}
+__device__ __forceinline__ void sgd1_any(const FcSegs& s, int64_t e, float S, float& w, float& v,
+                                         float lr, float mu, float wd, float inv_b) {
+    if (s.nseg > 0) sgd1_seg(s, e, S, w, v, lr, mu, wd, inv_b);
+    else sgd1(S, w, v, lr, mu, wd, inv_b);
+}
+
 __device__ __forceinline__ float4 add4(const float4& a, const float4& b) {
     return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
                        __fadd_rn(a.w, b.w));

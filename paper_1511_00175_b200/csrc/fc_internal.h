@@ -34,6 +34,14 @@ static inline FcFlagLayout fc_flag_layout(int64_t heap_bytes) {
     return L;
 }
 
+// Device copy of a Caffe per-blob multiplier table (nseg == 0: uniform update).
+struct FcSegs {
+    const int64_t* begin;
+    const float* lrm;
+    const float* dm;
+    int nseg;
+};
+
 // Everything a collective kernel needs to find every rank's buffers.
 struct FcPeers {
     char* heap[FC_MAX_RANKS];  // each rank's heap base, as mapped in this process
@@ -54,6 +62,7 @@ struct FcColl {
     int64_t off_mom;   // >= 0: mom is symmetric in the heap; < 0: use mom_local
     float* mom_local;
     float lr, mu, wd, inv_b;
+    FcSegs segs;       // per-blob multipliers for the fused update
     int bcast;         // fc_bcast
     int64_t bar_words, red_words, max_chunks;
     uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]

@@ -14,7 +14,7 @@ struct DevInfo {
 const DevInfo& dev_info();  // current device's SM count (cached per device)
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
-                            float wd, float inv_b, cudaStream_t st);
+                            float wd, float inv_b, const FcSegs& segs, cudaStream_t st);
 void set_sgd_unroll(int u);
 
 // Collective launch: `virt` -> one cooperative grid of (grid_x, p) CTAs that emulates all ranks.

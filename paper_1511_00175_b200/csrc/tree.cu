@@ -210,7 +210,7 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
         const int k = j * TREE_T + t;
         if (k < nf4) {
             const float4 s = add4(a[j], b[j]);
-            sgd4(s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+            sgd4_any(c.segs, e0 + 4 * (int64_t)k, s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
             st_na(w4 + k, w[j]);
             st_na(v4 + k, v[j]);
             if (direct) {
@@ -226,7 +226,7 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
         float* wp = w_of(c, rank) + e;
         float* vp = mom_of(c, rank) + e;
         float ww = *wp, vv = *vp;
-        sgd1(s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+        sgd1_any(c.segs, e, s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
         st1(wp, ww);
         st1(vp, vv);
         if (direct)
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                         const int64_t i = base + j * T;
                         if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
-                            sgd4(S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                            sgd4_any(c.segs, 4 * i, S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
                             st_na(v4 + i, v[j]);
 #pragma unroll
                             for (int q = 0; q < P; ++q)
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                 const float S = tree_sum_regs1<P, K>(xs);
                 if (fused) {
                     float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
-                    sgd1(S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                    sgd1_any(c.segs, e, S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
                     st1(mom_of(c, rank) + e, vv);
                     for (int q = 0; q < P; ++q) st1(w_of(c, q) + e, ww);
                 } else {

@@ -89,6 +89,47 @@ def test_forest_slices_are_bit_reversed_binomial_roots():
     assert order == [0, 4, 2, 6, 1, 5, 3, 7]
 
 
+@pytest.mark.parametrize("policy,kw", [
+    ("fixed", {}),
+    ("step", dict(gamma=0.1, stepsize=1000)),
+    ("multistep", dict(gamma=0.1, steps=(100_000, 200_000))),  # NiN
+    ("poly", dict(power=0.5, max_iter=450_000)),               # GoogLeNet
+])
+def test_lr_schedules_match_oracle(policy, kw):
+    import oracle
+
+    for base in (0.01, 0.04, 0.08):
+        for it in [0, 1, 999, 1000, 99_999, 100_000, 150_000, 200_000, 449_999, 450_000]:
+            if policy == "poly" and it > kw["max_iter"]:
+                continue
+            assert fc.firecaffe_lr_at(policy, base, it, **kw) == oracle.lr_at(policy, base, it, **kw)
+
+
+def test_lr_schedule_errors():
+    with pytest.raises(ValueError):
+        fc.firecaffe_lr_at("poly", 0.01, 11, max_iter=10)
+    with pytest.raises(ValueError):
+        fc.firecaffe_lr_at("step", 0.01, 5, stepsize=0)
+    with pytest.raises(ValueError):
+        fc.firecaffe_lr_at("fixed", 0.01, -1)
+
+
+def test_segment_table_validation_is_host_side():
+    import ctypes
+
+    L = _lib.load()
+    h = ctypes.c_void_p()
+
+    def make(rows, n):
+        arr = (_lib.FcSegment * len(rows))(*[_lib.FcSegment(*r) for r in rows])
+        return L.firecaffe_segments_create(arr, len(rows), n, ctypes.byref(h))
+
+    bad = [([(1, 1.0, 1.0)], 10), ([(0, 1.0, 1.0), (0, 2.0, 0.0)], 10), ([(0, 1.0, 1.0), (10, 2.0, 0.0)], 10),
+           ([(0, -1.0, 1.0)], 10), ([(0, 1.0, float("nan"))], 10), ([(0, 1.0, 1.0), (5, 1.0, 1.0), (3, 1.0, 1.0)], 10)]
+    for rows, n in bad:
+        assert make(rows, n) == _lib.FC_ERR_INVALID_ARG, rows
+
+
 def test_host_argument_errors_without_gpu():
     L = _lib.load()
     # n < 0 and bad hyper-parameters are rejected before any CUDA call

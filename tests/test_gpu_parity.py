@@ -282,6 +282,59 @@ def test_virtual_tolerance_vs_float64():
         W.close()
 
 
+@pytest.mark.parametrize("n", [5, 4097, 100_003, (1 << 20) + 3])
+def test_sgd_step_segments_bitexact(n):
+    """Caffe per-blob lr_mult / decay_mult (reading R20), ragged blob boundaries."""
+    begins, lm, dm = fc_inputs.caffe_blobs(n)
+    segs = fc.Segments(begins, lm, dm, n)
+    g = fc_inputs.grad(n, 0, seed=n + 11, dist="mixed")
+    w, v = fc_inputs.weights(n, seed=12), fc_inputs.momentum(n, seed=13)
+    wd_, vd = w.cuda(), v.cuda()
+    fc.firecaffe_sgd_step_segments(wd_, g.cuda(), vd, 0.04, 0.9, 5e-4, 1024, segs)
+    w_ref, v_ref = oracle.sgd_segments(w.numpy(), v.numpy(), g.numpy(), 0.04, 0.9, 5e-4, 1024, begins, lm, dm)
+    assert_bitexact(wd_, w_ref, "w")
+    assert_bitexact(vd, v_ref, "v")
+    # all multipliers 1 == plain sgd_step (bitwise)
+    ones = fc.Segments(begins, [1.0] * len(begins), [1.0] * len(begins), n)
+    w1, v1 = w.cuda(), v.cuda()
+    fc.firecaffe_sgd_step_segments(w1, g.cuda(), v1, 0.04, 0.9, 5e-4, 1024, ones)
+    w2, v2 = w.cuda(), v.cuda()
+    fc.firecaffe_sgd_step(w2, g.cuda(), v2, 0.04, 0.9, 5e-4, 1024)
+    assert_bitexact(w1, w2.cpu().numpy(), "ones w")
+    assert_bitexact(v1, v2.cpu().numpy(), "ones v")
+    with pytest.raises(fc.FcError):  # table built for another n
+        fc.firecaffe_sgd_step_segments(wd_, g.cuda(), vd, 0.04, 0.9, 5e-4, 1024, segs, n=n - 1)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree"), ("single_root", "direct")])
+def test_virtual_fused_segments_bitexact(p, sched, bcast):
+    if not _sched_ok(p, sched):
+        pytest.skip("forest needs a power-of-two world")
+    n = 3 * 4096 * p + 13
+    begins, lm, dm = fc_inputs.caffe_blobs(n)
+    segs = fc.Segments(begins, lm, dm, n)
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=6000 + p)
+        w0, v0 = fc_inputs.weights(n, seed=3), fc_inputs.momentum(n, seed=4)
+        _fill(grads, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd_segments(ws[0], grads[0], moms[0], 0.08, 0.9, 2e-4, 1024, segs, W)
+        assert W.poll() == 0
+        S = oracle.tree_sum(g.numpy(), 2)
+        w_ref, v_ref = oracle.sgd_segments(w0.numpy(), v0.numpy(), S, 0.08, 0.9, 2e-4, 1024, begins, lm, dm)
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            assert_bitexact(moms[r][b:e], v_ref[b:e], f"mom rank {r}")
+    finally:
+        W.close()
+
+
 def test_virtual_rejects_non_symmetric_buffers():
     W = _world(2, 1000, bufs=1)
     try:

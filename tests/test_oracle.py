@@ -280,3 +280,67 @@ def test_subnormals_preserved():
     a = [g[r] for r in range(4)]
     np.testing.assert_array_equal(s.view(np.uint32), ((a[0] + a[1]) + (a[2] + a[3])).view(np.uint32))
     assert np.any((s != 0) & (np.abs(s) < np.finfo(np.float32).tiny))
+
+
+# --------------------------------------------------------------------------
+# f2: Caffe per-blob multipliers and LR schedules (readings R20, R21)
+# --------------------------------------------------------------------------
+def test_segments_all_ones_is_plain_sgd():
+    n = 50_001
+    g = _rand(1, n, seed=31)[0]
+    w = fc_inputs.weights(n, seed=32).numpy()
+    v = fc_inputs.momentum(n, seed=33).numpy()
+    ref = oracle.sgd(w, v, g, 0.04, 0.9, 5e-4, 1024)
+    got = oracle.sgd_segments(w, v, g, 0.04, 0.9, 5e-4, 1024, [0, 1000, 20_000], [1, 1, 1], [1, 1, 1])
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_segments_caffe_weight_and_bias_by_hand():
+    # blob 0: weights (lr_mult 1, decay_mult 1) -> SPEC S:91 example: 0.94 / 0.06
+    # blob 1: bias    (lr_mult 2, decay_mult 0) -> v' = 0.2*0.5 = 0.1, w' = 0.9
+    w, v = oracle.sgd_segments([1.0, 1.0], [0.0, 0.0], [0.5, 0.5], 0.1, 0.9, 0.1, 1, [0, 1], [1, 2], [1, 0])
+    assert abs(float(w[0]) - 0.94) <= float(_ulp(0.94)) and abs(float(v[0]) - 0.06) <= float(_ulp(0.06))
+    assert abs(float(w[1]) - 0.9) <= float(_ulp(0.9)) and abs(float(v[1]) - 0.1) <= float(_ulp(0.1))
+
+
+def test_segments_equal_plain_sgd_per_blob_with_scaled_hyper():
+    n = 30_000
+    g = _rand(1, n, seed=41, dist="mixed")[0]
+    w = fc_inputs.weights(n, seed=42).numpy()
+    v = fc_inputs.momentum(n, seed=43).numpy()
+    begins, lm, dm = [0, 7, 5000, 5001, 17_777], [1.0, 2.0, 0.5, 10.0, 1.0], [1.0, 0.0, 3.0, 0.0, 0.25]
+    lr, mu, wd, B = 0.04, 0.9, 5e-4, 1024
+    gw, gv = oracle.sgd_segments(w, v, g, lr, mu, wd, B, begins, lm, dm)
+    ends = begins[1:] + [n]
+    for b, e, a, d in zip(begins, ends, lm, dm):
+        rw, rv = oracle.sgd(w[b:e], v[b:e], g[b:e], float(np.float32(lr) * np.float32(a)), mu,
+                            float(np.float32(wd) * np.float32(d)), B)
+        np.testing.assert_array_equal(gw[b:e].view(np.uint32), rw.view(np.uint32))
+        np.testing.assert_array_equal(gv[b:e].view(np.uint32), rv.view(np.uint32))
+
+
+def test_segments_reject_bad_tables():
+    z = np.zeros(10, np.float32)
+    for begins in ([1], [0, 0], [0, 5, 3], [0, 10]):
+        with pytest.raises(ValueError):
+            oracle.sgd_segments(z, z, z, 0.1, 0.9, 0.0, 1, begins, [1] * len(begins), [1] * len(begins))
+
+
+def test_lr_schedules_spec_and_paper_values():
+    # SPEC S:107-109 (poly, power 0.5 per P:452)
+    assert oracle.lr_at("poly", 0.01, 0, max_iter=1000) == np.float32(0.01)
+    assert oracle.lr_at("poly", 0.01, 1000, max_iter=1000) == 0.0
+    assert abs(oracle.lr_at("poly", 0.01, 500, max_iter=1000) - 0.0070711) < 1e-7
+    # P:407 NiN: 0.01, "reduce this by a factor of 10x twice"
+    st = dict(gamma=0.1, steps=(100_000, 200_000))
+    assert oracle.lr_at("multistep", 0.01, 99_999, **st) == np.float32(0.01)
+    assert abs(oracle.lr_at("multistep", 0.01, 100_000, **st) - 0.001) <= float(_ulp(0.001))
+    assert abs(oracle.lr_at("multistep", 0.01, 250_000, **st) - 0.0001) <= float(_ulp(0.0001))
+    assert oracle.lr_at("step", 0.04, 25, gamma=0.5, stepsize=10) == np.float32(0.01)
+    assert oracle.lr_at("fixed", 0.08, 123) == np.float32(0.08)
+    with pytest.raises(ValueError):
+        oracle.lr_at("poly", 0.01, 1001, max_iter=1000)
+    # poly is non-increasing (SPEC invariant)
+    vals = [oracle.lr_at("poly", 0.08, i, max_iter=97) for i in range(98)]
+    assert all(a >= b for a, b in zip(vals, vals[1:]))
