@@ -132,10 +132,21 @@ __device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
     return __syncthreads_and(good) != 0;
 }
 
-// After the CTA finished writing a chunk: publish it with one flag.
-__device__ __forceinline__ void signal_one(const FcColl& c, uint32_t* f) {
+// Publish the CTA's last `count` chunks (cc_last, cc_last - G, ...) after ONE
+// sys-scope release fence: thread 0 fences (ordering every thread's chunk
+// writes, sequenced before it by the bar.sync) and then writes the consumers'
+// epoch stamps with relaxed stores (`stamp(cc)` does the stores for one
+// chunk).  A sys fence costs 4-8 us on B200 (scripts/fence_bench.cu), so the
+// tree schedules pay one per PUB chunks instead of one per chunk.
+constexpr int PUB = 8;
+template <typename Stamp>
+__device__ __forceinline__ void publish_batch(const FcColl& c, int64_t cc_last, int G, int count,
+                                              Stamp stamp) {
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(f, c.epoch);
+    if (threadIdx.x == 0) {
+        fence_sys();
+        for (int k = 0; k < count; ++k) stamp(cc_last - (int64_t)k * G);
+    }
 }
 
 __device__ __forceinline__ int64_t first_chunk(int64_t lo, int G, int b) {
@@ -389,12 +400,21 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
         const int64_t mid_next = lo + (hi - lo + 1) / 2;
         const bool keep_lower_next = ((rank >> (l + 1)) & 1) == 0;
         const float* pg = grad_of(c, partner);
+        const int next_partner = rank ^ (1 << (l + 1));
+        auto stamp = [&](int64_t cx) {  // next-level consumer of chunk cx is the partner
+            if ((cx < mid_next) != keep_lower_next) st_relaxed_sys(red_flag(c, next_partner, l, cx), c.epoch);
+        };
+        int pend = 0;
+        int64_t cc_last = -1;
         for (int64_t cc = first_chunk(lo, G, b); cc < hi; cc += G) {
             if (l >= 1 && !wait_one(c, red_flag(c, rank, l - 1, cc))) { ok = false; break; }
             reduce_chunk<P>(c, rank, cc, own, pg, last, fused, direct);
-            if (!last && ((cc < mid_next) != keep_lower_next))  // next-level consumer is the partner
-                signal_one(c, red_flag(c, rank ^ (1 << (l + 1)), l, cc));
+            if (!last) {
+                cc_last = cc;
+                if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
+            }
         }
+        if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
     }
 
     // ---- broadcast back down the tree (recursive doubling), or direct
@@ -411,12 +431,17 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
                 if ((rank >> i) & 1) rlo = m2; else rhi = m2;
             }
             float* dst = fused ? w_of(c, partner) : grad_of(c, partner);
+            auto stamp = [&](int64_t cx) { st_relaxed_sys(av_flag(c, partner, cx), c.epoch); };
+            int pend = 0;
+            int64_t cc_last = -1;
             for (int64_t cc = first_chunk(rlo, G, b); cc < rhi; cc += G) {
                 const bool owned = cc >= o0 && cc < o1;
                 if (!owned && !wait_one(c, av_flag(c, rank, cc))) { ok = false; break; }
                 copy_chunk(c, cc, mine, &dst, 1);
-                signal_one(c, av_flag(c, partner, cc));
+                cc_last = cc;
+                if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
             }
+            if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
         }
         if (ok && M > 0) {  // chunks that arrive at the last level are not forwarded: wait for them
             const int p0 = rank ^ 1;
@@ -464,11 +489,18 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         const bool root_final = (rank == 0) && (l == L - 1);
         const bool signal_parent = (l == last_recv) && (parent >= 0);
         const float* cg = grad_of(c, child);
+        auto stamp = [&](int64_t cx) { st_relaxed_sys(red_flag(c, parent, send_level, cx), c.epoch); };
+        int pend = 0;
+        int64_t cc_last = -1;
         for (int64_t cc = b; cc < nch; cc += G) {
             if (child_has_children && !wait_one(c, red_flag(c, rank, l, cc))) { ok = false; break; }
             reduce_chunk<P>(c, rank, cc, own, cg, root_final, fused, direct);
-            if (signal_parent) signal_one(c, red_flag(c, parent, send_level, cc));
+            if (signal_parent) {
+                cc_last = cc;
+                if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
+            }
         }
+        if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
     }
 
     trace(c, 2);
@@ -480,19 +512,21 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         const int top = rank == 0 ? L : send_level;
         for (int l = top - 1; l >= 0; --l)
             if (rank + (1 << l) < P) dst[nd++] = fused ? w_of(c, rank + (1 << l)) : grad_of(c, rank + (1 << l));
+        auto stamp = [&](int64_t cx) {
+            for (int l = top - 1; l >= 0; --l)
+                if (rank + (1 << l) < P) st_relaxed_sys(av_flag(c, rank + (1 << l), cx), c.epoch);
+        };
+        int pend = 0;
+        int64_t cc_last = -1;
         for (int64_t cc = b; cc < nch && ok; cc += G) {
             if (rank != 0 && !wait_one(c, av_flag(c, rank, cc))) { ok = false; break; }
             if (nd > 0) {
                 copy_chunk(c, cc, mine, dst, nd);
-                __syncthreads();
-                if (threadIdx.x < nd) {
-                    int child = -1, k = 0;
-                    for (int l = top - 1; l >= 0; --l)
-                        if (rank + (1 << l) < P) { if (k == (int)threadIdx.x) child = rank + (1 << l); ++k; }
-                    st_release_sys(av_flag(c, child, cc), c.epoch);
-                }
+                cc_last = cc;
+                if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
             }
         }
+        if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
     } else {
         cta_barrier(c, rank, 1);
     }
