@@ -387,10 +387,11 @@ def main():
     g_host = g0.cpu().pin_memory()
     w_host = torch.empty(n, dtype=torch.float32).pin_memory()
 
-    def e2e_step():
-        grad.copy_(g_host, non_blocking=True)
-        step()
-        w_host.copy_(w, non_blocking=True)
+    def e2e_step():  # the library's host-buffer entry points (copies inside the C call)
+        if N > 1:
+            fc.firecaffe_tree_allreduce_sgd_host(w, grad, mom, g_host, w_host, world=W, **hp)
+        else:
+            fc.firecaffe_sgd_step_host(w, grad, mom, g_host, w_host, **hp)
 
     reset()
     e2e_ms, _, _ = timed(e2e_step, max(5, min(args.steps, 50)), min(args.warmup, 5))
@@ -485,7 +486,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_ms, 4),
-                    "what": "pinned host grad -> device, the step, updated w -> pinned host"},
+                    "what": ("firecaffe_sgd_step_host: pinned host grad -> device, SGD, updated w -> pinned "
+                             "host, chunk-pipelined (H2D || SGD || D2H)") if N == 1 else
+                            "firecaffe_tree_allreduce_sgd_host: pinned host grad -> heap, fused tree, w -> host"},
             "gpu_launches": args.steps,
             "gpu_launches_note": "one library kernel per step (L2-flush and barrier kernels are torch/NCCL)",
             "clocks": clocks,

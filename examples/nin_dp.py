@@ -94,6 +94,8 @@ def run(p: int = 4, B: int = 64, steps: int = 5, lr: float = 0.04, mu: float = 0
     reference.  Returns (per-rank weights list, reference weights, losses)."""
     torch.backends.cudnn.deterministic = True
     torch.backends.cudnn.benchmark = False
+    torch.backends.cudnn.allow_tf32 = False  # fp32 convolutions, as Caffe (P:508: fp32 throughout)
+    torch.backends.cuda.matmul.allow_tf32 = False
     dev = torch.device("cuda", torch.cuda.current_device())
     replicas = [make_nin(0).to(dev) for _ in range(p)]
     ref = make_nin(0).to(dev)

@@ -221,6 +221,29 @@ fc_status firecaffe_tree_allreduce_sgd_segments(float* w, float* grad, float* mo
                                                 const fc_segments* segs, fc_world* world,
                                                 void* stream);
 
+/* ------------------------------------------------ host-buffer entry points
+ * The same operations fed from / returned to HOST memory, for callers whose
+ * gradients live on the host (and for the end-to-end benchmark).  grad_host
+ * and w_host must be page-locked (cudaMallocHost / cudaHostRegister), n floats
+ * each; w, grad, mom are the usual device buffers (grad receives the copy).
+ * firecaffe_sgd_step_host: chunked pipeline over internal streams (H2D of
+ *   chunk i+1 || SGD of chunk i || D2H of chunk i-1; PCIe is full duplex);
+ *   results identical to firecaffe_sgd_step.  Ordered after prior work on
+ *   `stream`; later work on `stream` sees every copy complete.  Not re-entrant
+ *   across host threads on the same device.
+ * firecaffe_tree_allreduce_sgd_host: H2D into the symmetric grad, the fused
+ *   collective, D2H of the updated weights, on `stream`.
+ * segs may be NULL (uniform multipliers).  Errors as the device versions, plus
+ * FC_ERR_INVALID_ARG for host buffers that are not page-locked. */
+fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float* grad_host,
+                                  float* w_host, int64_t n, float lr, float mu, float wd,
+                                  int64_t batch, const fc_segments* segs, void* stream);
+fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
+                                            const float* grad_host, float* w_host, int64_t n,
+                                            float lr, float mu, float wd, int64_t batch,
+                                            const fc_segments* segs, fc_world* world,
+                                            void* stream);
+
 /* ------------------------------------------------ learning-rate schedules
  * The paper's schedules (R21): FIXED; STEP gamma^floor(iter/stepsize);
  * MULTISTEP gamma^#{steps[k] <= iter} ("reduce this by a factor of 10x twice",

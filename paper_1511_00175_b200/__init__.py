@@ -143,6 +143,30 @@ def firecaffe_tree_allreduce_sgd_segments(w, grad, mom, lr, mu, wd, batch, segs:
           "firecaffe_tree_allreduce_sgd_segments")
 
 
+def _hptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    if x.is_cuda or not x.is_pinned() or not x.is_contiguous():
+        raise ValueError("host buffers must be contiguous pinned CPU tensors")
+    return x.data_ptr()
+
+
+def firecaffe_sgd_step_host(w, grad, mom, grad_host, w_host, lr, mu, wd, batch, segs=None, n=None, stream=None):
+    """firecaffe_sgd_step fed from pinned host memory, pipelined H2D || SGD || D2H."""
+    check(load().firecaffe_sgd_step_host(_ptr(w), _ptr(grad), _ptr(mom), _hptr(grad_host), _hptr(w_host),
+                                         _numel(n, w), lr, mu, wd, int(batch), segs.handle if segs else None,
+                                         _stream(stream)), "firecaffe_sgd_step_host")
+
+
+def firecaffe_tree_allreduce_sgd_host(w, grad, mom, grad_host, w_host, lr, mu, wd, batch, world: "World",
+                                      segs=None, n=None, stream=None):
+    """firecaffe_tree_allreduce_sgd with the gradient from / weights to pinned host memory."""
+    check(load().firecaffe_tree_allreduce_sgd_host(_ptr(w), _ptr(grad), _ptr(mom), _hptr(grad_host),
+                                                   _hptr(w_host), _numel(n, w), lr, mu, wd, int(batch),
+                                                   segs.handle if segs else None, world.handle, _stream(stream)),
+          "firecaffe_tree_allreduce_sgd_host")
+
+
 def firecaffe_lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, stepsize: int = 0, steps=(),
                     power: float = 0.5, max_iter: int = 0) -> float:
     """Learning rate of the paper's schedules at iteration `it` (header: firecaffe_lr_at)."""

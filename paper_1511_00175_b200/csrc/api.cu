@@ -540,6 +540,62 @@ fc_status firecaffe_segments_destroy(fc_segments* t) {
     return FC_OK;
 }
 
+static bool pinned_host(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float* grad_host,
+                                  float* w_host, int64_t n, float lr, float mu, float wd,
+                                  int64_t batch, const fc_segments* segs, void* stream) {
+    if (n < 0) return FC_ERR_INVALID_ARG;
+    fc_status st = check_hyper(lr, mu, wd, batch);
+    if (st != FC_OK) return st;
+    if (n == 0) return FC_OK;
+    if (check_vec(w, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    if (!grad_host || !w_host || !pinned_host(grad_host) || !pinned_host(w_host))
+        return FC_ERR_INVALID_ARG;
+    const int64_t bytes = n * 4;
+    if (overlap(w, grad, bytes) || overlap(w, mom, bytes) || overlap(grad, mom, bytes) ||
+        overlap(grad_host, w_host, bytes))
+        return FC_ERR_INVALID_ARG;
+    FcSegs sd;
+    st = check_segs(segs, n, &sd);
+    if (st != FC_OK) return st;
+    const int64_t chunk = (int64_t)1 << 20;  // 4 MB per stage: ~75 us of PCIe each way
+    cudaError_t e = launch_sgd_step_host(w, grad_host, grad, mom, w_host, n, lr, mu, wd,
+                                         inv_batch(batch), sd, chunk, (cudaStream_t)stream);
+    return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
+}
+
+fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
+                                            const float* grad_host, float* w_host, int64_t n,
+                                            float lr, float mu, float wd, int64_t batch,
+                                            const fc_segments* segs, fc_world* world,
+                                            void* stream) {
+    if (!world || n < 0) return FC_ERR_INVALID_ARG;
+    if (world->virt) return FC_ERR_UNSUPPORTED;  // one host buffer cannot feed p virtual ranks
+    if (world->p == 1)
+        return firecaffe_sgd_step_host(w, grad, mom, grad_host, w_host, n, lr, mu, wd, batch, segs,
+                                       stream);
+    if (n == 0) return FC_OK;
+    if (!grad_host || !w_host || !pinned_host(grad_host) || !pinned_host(w_host))
+        return FC_ERR_INVALID_ARG;
+    if (check_vec(grad, n) || check_vec(w, n)) return FC_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(grad, grad_host, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return FC_ERR_CUDA;
+    fc_status st = fused_impl(w, grad, mom, n, lr, mu, wd, batch, segs, world, stream);
+    if (st != FC_OK) return st;
+    if (cudaMemcpyAsync(w_host, w, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return FC_ERR_CUDA;
+    return FC_OK;
+}
+
 // The paper's learning-rate schedules, in double, one
 // rounding to fp32 (R21).
 float firecaffe_lr_at(const fc_lr_schedule* s, int64_t iter) {

@@ -15,7 +15,17 @@ const DevInfo& dev_info();  // current device's SM count (cached per device)
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
                             float wd, float inv_b, const FcSegs& segs, cudaStream_t st);
+cudaError_t launch_sgd_step_range(float* w, const float* grad, float* mom, int64_t off, int64_t len,
+                                  float lr, float mu, float wd, float inv_b, const FcSegs& segs,
+                                  cudaStream_t st);
 void set_sgd_unroll(int u);
+
+// Host-buffer pipeline (host_pipeline.cu)
+constexpr int kPipeDepth = 4;
+cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_dev, float* mom,
+                                 float* w_host, int64_t n, float lr, float mu, float wd,
+                                 float inv_b, const FcSegs& segs, int64_t chunk,
+                                 cudaStream_t user);
 
 // Collective launch: `virt` -> one cooperative grid of (grid_x, p) CTAs that emulates all ranks.
 cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,

@@ -1,0 +1,83 @@
+// Host-buffer entry points: the 1-GPU fused SGD with the gradient coming from
+// (pinned) host memory and the updated weights going back to it, pipelined in
+// chunks over three streams so that the H2D copy of chunk i+1, the SGD kernel
+// of chunk i and the D2H copy of chunk i-1 overlap (PCIe is full duplex: the
+// two copy directions run on separate copy engines).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fc_internal.h"
+#include "fc_launch.h"
+
+namespace fc {
+
+struct PipeCtx {
+    bool ready = false;
+    cudaStream_t s[3];             // 0: H2D, 1: compute, 2: D2H
+    cudaEvent_t start;             // user stream -> internal streams
+    cudaEvent_t h2d[kPipeDepth], comp[kPipeDepth], d2h[kPipeDepth];
+};
+
+static PipeCtx g_pipe[64];
+
+static cudaError_t pipe_ctx(PipeCtx** out) {
+    int d = 0;
+    cudaError_t e = cudaGetDevice(&d);
+    if (e != cudaSuccess) return e;
+    if (d < 0 || d >= 64) return cudaErrorInvalidDevice;
+    PipeCtx& p = g_pipe[d];
+    if (!p.ready) {
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaStreamCreateWithFlags(&p.s[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming)) != cudaSuccess) return e;
+        for (int i = 0; i < kPipeDepth; ++i) {
+            if ((e = cudaEventCreateWithFlags(&p.h2d[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&p.comp[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&p.d2h[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        p.ready = true;
+    }
+    *out = &p;
+    return cudaSuccess;
+}
+
+cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_dev, float* mom,
+                                 float* w_host, int64_t n, float lr, float mu, float wd,
+                                 float inv_b, const FcSegs& segs, int64_t chunk,
+                                 cudaStream_t user) {
+    PipeCtx* p = nullptr;
+    cudaError_t e = pipe_ctx(&p);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(p->start, user)) != cudaSuccess) return e;
+    for (int i = 0; i < 3; ++i)
+        if ((e = cudaStreamWaitEvent(p->s[i], p->start, 0)) != cudaSuccess) return e;
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    for (int64_t k = 0; k < nchunks; ++k) {
+        const int64_t off = k * chunk;
+        const int64_t len = (off + chunk <= n) ? chunk : n - off;
+        const int slot = (int)(k % kPipeDepth);
+        // H2D of chunk k (reuses staging only through grad_dev, which is per-chunk disjoint)
+        if ((e = cudaMemcpyAsync(grad_dev + off, grad_host + off, len * 4, cudaMemcpyHostToDevice,
+                                 p->s[0])) != cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(p->h2d[slot], p->s[0])) != cudaSuccess) return e;
+        // SGD on chunk k
+        if ((e = cudaStreamWaitEvent(p->s[1], p->h2d[slot], 0)) != cudaSuccess) return e;
+        FcSegs sub = segs;  // the blob table is indexed by absolute element: shift the base
+        if ((e = launch_sgd_step_range(w, grad_dev, mom, off, len, lr, mu, wd, inv_b, sub, p->s[1])) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(p->comp[slot], p->s[1])) != cudaSuccess) return e;
+        // D2H of chunk k's updated weights
+        if ((e = cudaStreamWaitEvent(p->s[2], p->comp[slot], 0)) != cudaSuccess) return e;
+        if ((e = cudaMemcpyAsync(w_host + off, w + off, len * 4, cudaMemcpyDeviceToHost, p->s[2])) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(p->d2h[slot], p->s[2])) != cudaSuccess) return e;
+    }
+    // the user's stream continues after every copy has landed
+    if ((e = cudaEventRecord(p->start, p->s[2])) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(user, p->start, 0);
+}
+
+}  // namespace fc

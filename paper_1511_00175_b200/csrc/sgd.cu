@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                                                        const float* __restrict__ gt,
                                                        float* __restrict__ vt, int tail, float lr,
                                                        float mu, float wd, float inv_b,
-                                                       const FcSegs segs) {
+                                                       const FcSegs segs, int64_t elem0) {
     const int64_t T = blockDim.x;
     const int64_t stride = (int64_t)gridDim.x * T * U;
     for (int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x; base < n4; base += stride) {
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
         for (int j = 0; j < U; ++j) {
             const int64_t i = base + j * T;
             if (i < n4) {
-                sgd4_any(segs, 4 * i, g[j], w[j], v[j], lr, mu, wd, inv_b);
+                sgd4_any(segs, elem0 + 4 * i, g[j], w[j], v[j], lr, mu, wd, inv_b);
                 st_na(w4 + i, w[j]);
                 st_na(v4 + i, v[j]);
             }
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < tail) {
         const int t = threadIdx.x;
         float w = wt[t], v = vt[t];
-        sgd1_any(segs, 4 * n4 + t, gt[t], w, v, lr, mu, wd, inv_b);
+        sgd1_any(segs, elem0 + 4 * n4 + t, gt[t], w, v, lr, mu, wd, inv_b);
         wt[t] = w;
         vt[t] = v;
     }
@@ -57,6 +57,17 @@ static int g_sgd_unroll = 4;
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
                             float wd, float inv_b, const FcSegs& segs, cudaStream_t st) {
+    return launch_sgd_step_range(w, grad, mom, 0, n, lr, mu, wd, inv_b, segs, st);
+}
+
+// Elements [off, off + len) (off a multiple of 4); blob lookups use absolute indices.
+cudaError_t launch_sgd_step_range(float* w0, const float* grad0, float* mom0, int64_t off,
+                                  int64_t len, float lr, float mu, float wd, float inv_b,
+                                  const FcSegs& segs, cudaStream_t st) {
+    float* w = w0 + off;
+    const float* grad = grad0 + off;
+    float* mom = mom0 + off;
+    const int64_t n = len;
     const int64_t n4 = n / 4;
     const int tail = (int)(n - n4 * 4);
     const int T = 256;
@@ -71,7 +82,7 @@ cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, 
         if (grid < 1) grid = 1;
         kern<<<(unsigned)grid, T, 0, st>>>((float4*)w, (const float4*)grad, (float4*)mom, n4,
                                            w + n4 * 4, grad + n4 * 4, mom + n4 * 4, tail, lr, mu,
-                                           wd, inv_b, segs);
+                                           wd, inv_b, segs, off);
         return cudaGetLastError();
     };
     switch (g_sgd_unroll) {

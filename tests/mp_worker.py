@@ -74,6 +74,16 @@ def main():
         torch.cuda.synchronize()
         if not np.array_equal(bits(grad[:n]), ps_ref.view(np.uint32)):
             fails.append(f"ps n={n}")
+        # host-buffer entry point (pinned grad in, pinned weights out)
+        W.config("flat", "direct", 2)
+        g_host = g_all[rank].clone().pin_memory()
+        w_host = torch.empty(n, dtype=torch.float32).pin_memory()
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        fc.firecaffe_tree_allreduce_sgd_host(w, grad, mom, g_host, w_host, world=W, n=n, **HP)
+        torch.cuda.synchronize()
+        if not np.array_equal(w_host.numpy().view(np.uint32), w_ref.view(np.uint32)):
+            fails.append(f"host entry w n={n}")
     st = W.poll()
     if st != 0:
         fails.append(f"device status {st}")

@@ -335,6 +335,33 @@ def test_virtual_fused_segments_bitexact(p, sched, bcast):
         W.close()
 
 
+@pytest.mark.parametrize("n", [3, 4096 + 1, 3 * (1 << 20) + 7])
+@pytest.mark.parametrize("with_segs", [False, True])
+def test_sgd_step_host_pipeline_bitexact(n, with_segs):
+    """Host-buffer entry point: chunked H2D || SGD || D2H gives sgd_step's bits."""
+    g = fc_inputs.grad(n, 0, seed=n + 21)
+    w, v = fc_inputs.weights(n, seed=22), fc_inputs.momentum(n, seed=23)
+    g_host = g.pin_memory()
+    w_host = torch.empty(n, dtype=torch.float32).pin_memory()
+    w_dev, v_dev, g_dev = w.cuda(), v.cuda(), torch.empty(n, device="cuda")
+    segs = None
+    if with_segs:
+        b, lm, dm = fc_inputs.caffe_blobs(n)
+        segs = fc.Segments(b, lm, dm, n)
+        w_ref, v_ref = oracle.sgd_segments(w.numpy(), v.numpy(), g.numpy(), **HYPER, begins=b, lr_mults=lm,
+                                           decay_mults=dm)
+    else:
+        w_ref, v_ref = oracle.sgd(w.numpy(), v.numpy(), g.numpy(), **HYPER)
+    fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g_host, w_host, **HYPER, segs=segs)
+    torch.cuda.current_stream().synchronize()
+    assert_bitexact(w_host, w_ref, "w_host")
+    assert_bitexact(w_dev, w_ref, "w")
+    assert_bitexact(v_dev, v_ref, "v")
+    assert_bitexact(g_dev, g.numpy(), "grad copied")
+    with pytest.raises(ValueError):  # pageable host memory is refused
+        fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g, w_host, **HYPER)
+
+
 def test_virtual_rejects_non_symmetric_buffers():
     W = _world(2, 1000, bufs=1)
     try:
