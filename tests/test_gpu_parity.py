@@ -362,6 +362,55 @@ def test_sgd_step_host_pipeline_bitexact(n, with_segs):
         fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g, w_host, **HYPER)
 
 
+def test_sgd_step_vgg19_full_size_every_element():
+    """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
+    cfg = fc_inputs.CONFIGS["vgg19"]
+    n = cfg["n"]
+    hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
+    g = fc_inputs.grad(n, 0, device="cuda")
+    w = fc_inputs.weights(n, device="cuda")
+    v = fc_inputs.momentum(n, device="cuda")
+    gh, wh, vh = g.cpu().numpy(), w.cpu().numpy(), v.cpu().numpy()
+    fc.firecaffe_sgd_step(w, g, v, **hp)
+    w_ref, v_ref = oracle.sgd(wh, vh, gh, **hp)
+    assert_bitexact(w, w_ref, "w")
+    assert_bitexact(v, v_ref, "v")
+
+
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree")])
+def test_virtual_fused_vgg19_p8_sampled(sched, bcast):
+    """VGG-19 size, 8 ranks (virtual), default executor and the paper's forest: 8192
+    random indices + the ragged tail compared with the oracle, computed element by element."""
+    cfg = fc_inputs.CONFIGS["vgg19"]
+    n, p = cfg["n"], 8
+    hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        w0 = fc_inputs.weights(n, device="cuda")
+        v0 = fc_inputs.momentum(n, device="cuda")
+        for r in range(p):
+            grads[r].copy_(fc_inputs.grad(n, r, device="cuda"))
+            ws[r].copy_(w0)
+            moms[r].copy_(v0)
+        gen = torch.Generator().manual_seed(99)
+        idx = torch.cat([torch.randint(0, n, (8192,), generator=gen), torch.arange(n - 37, n)]).cuda()
+        G = torch.stack([grads[r][idx] for r in range(p)]).cpu().numpy()
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **hp)
+        assert W.poll() == 0
+        w_ref, v_ref = oracle.fused_step(G, w0[idx].cpu().numpy(), v0[idx].cpu().numpy(), **hp)
+        idx_c = idx.cpu()
+        for r in range(p):
+            assert_bitexact(ws[r][idx], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            own = ((idx_c >= b) & (idx_c < e)).numpy()
+            assert_bitexact(moms[r][idx].cpu().numpy()[own], v_ref[own], f"mom rank {r}")
+        assert torch.equal(ws[0], ws[p - 1])
+    finally:
+        W.close()
+
+
 def test_virtual_rejects_non_symmetric_buffers():
     W = _world(2, 1000, bufs=1)
     try:
