@@ -3,6 +3,7 @@
 // virtual world on one GPU), executor selection and kernel launch.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cmath>
@@ -566,7 +567,13 @@ fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float
     FcSegs sd;
     st = check_segs(segs, n, &sd);
     if (st != FC_OK) return st;
-    const int64_t chunk = (int64_t)1 << 20;  // 4 MB per stage: ~75 us of PCIe each way
+    static int64_t chunk = 0;  // floats per pipeline stage (FC_PIPE_CHUNK overrides, for tuning)
+    if (chunk == 0) {
+        const char* e = getenv("FC_PIPE_CHUNK");
+        chunk = e ? atoll(e) : ((int64_t)1 << 21);  // 8 MB stages (scripts/pcie_bench.py)
+        chunk = (chunk + 3) / 4 * 4;
+        if (chunk < 4096) chunk = 4096;
+    }
     cudaError_t e = launch_sgd_step_host(w, grad_host, grad, mom, w_host, n, lr, mu, wd,
                                          inv_batch(batch), sd, chunk, (cudaStream_t)stream);
     return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;

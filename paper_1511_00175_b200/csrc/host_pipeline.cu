@@ -51,10 +51,12 @@ cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_d
     if ((e = cudaEventRecord(p->start, user)) != cudaSuccess) return e;
     for (int i = 0; i < 3; ++i)
         if ((e = cudaStreamWaitEvent(p->s[i], p->start, 0)) != cudaSuccess) return e;
-    const int64_t nchunks = (n + chunk - 1) / chunk;
-    for (int64_t k = 0; k < nchunks; ++k) {
-        const int64_t off = k * chunk;
-        const int64_t len = (off + chunk <= n) ? chunk : n - off;
+    // Uniform stages (measured on B200, NiN: 2M-float stages 0.84 ms; 0.5M 0.96 ms;
+    // a small-first/small-last ramp did not help; H2D || D2H alone is 0.66 ms).
+    const int64_t nst = (n + chunk - 1) / chunk;
+    int64_t off = 0;
+    for (int64_t k = 0; k < nst; ++k) {
+        const int64_t len = off + chunk <= n ? chunk : n - off;
         const int slot = (int)(k % kPipeDepth);
         // H2D of chunk k (reuses staging only through grad_dev, which is per-chunk disjoint)
         if ((e = cudaMemcpyAsync(grad_dev + off, grad_host + off, len * 4, cudaMemcpyHostToDevice,
@@ -63,8 +65,8 @@ cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_d
         if ((e = cudaEventRecord(p->h2d[slot], p->s[0])) != cudaSuccess) return e;
         // SGD on chunk k
         if ((e = cudaStreamWaitEvent(p->s[1], p->h2d[slot], 0)) != cudaSuccess) return e;
-        FcSegs sub = segs;  // the blob table is indexed by absolute element: shift the base
-        if ((e = launch_sgd_step_range(w, grad_dev, mom, off, len, lr, mu, wd, inv_b, sub, p->s[1])) !=
+        // (the blob table is indexed by absolute element; the range launcher passes `off`)
+        if ((e = launch_sgd_step_range(w, grad_dev, mom, off, len, lr, mu, wd, inv_b, segs, p->s[1])) !=
             cudaSuccess)
             return e;
         if ((e = cudaEventRecord(p->comp[slot], p->s[1])) != cudaSuccess) return e;
@@ -74,6 +76,7 @@ cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_d
             cudaSuccess)
             return e;
         if ((e = cudaEventRecord(p->d2h[slot], p->s[2])) != cudaSuccess) return e;
+        off += len;
     }
     // the user's stream continues after every copy has landed
     if ((e = cudaEventRecord(p->start, p->s[2])) != cudaSuccess) return e;
