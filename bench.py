@@ -315,7 +315,7 @@ def main():
 
     # ---- buffers
     if N > 1:
-        W = fc.World.create(heap_bytes_for(3 * n + 4096))
+        W = fc.World.create(heap_bytes_for(3 * n + n // 2 + 8192))  # grad, w, mom (+ bf16 grad)
         if args.sched or args.bcast:
             c = W.get_config()
             W.config(args.sched or c["sched"], args.bcast or c["bcast"], 2)
@@ -448,6 +448,11 @@ def main():
             reset()
             baselines["nccl_allreduce+sgd_ms"] = round(timed(nccl_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
             baselines["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+            gb = W.alloc(n, "bf16")  # bf16 gradients on the wire (fp32 accumulate + update)
+            gb.copy_(g0.to(torch.bfloat16))
+            reset()
+            baselines["flat_bf16_wire_ms"] = round(
+                timed(lambda: fc.firecaffe_tree_allreduce_sgd_bf16(w, gb, mom, world=W, **hp), Kb, Wb)[0], 4)
         else:
             def torch_sgd():  # plain PyTorch ops of the same update (several kernels)
                 gg = grad * (1.0 / hp["batch"])
@@ -457,6 +462,10 @@ def main():
 
             reset()
             baselines["torch_eager_sgd_ms"] = round(timed(torch_sgd, Kb, Wb)[0], 4)
+            gb = g0.to(torch.bfloat16)
+            reset()
+            baselines["sgd_step_bf16_grad_ms"] = round(
+                timed(lambda: fc.firecaffe_sgd_step_bf16(w, gb, mom, **hp), Kb, Wb)[0], 4)
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
     cpu = None

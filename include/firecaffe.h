@@ -221,6 +221,25 @@ fc_status firecaffe_tree_allreduce_sgd_segments(float* w, float* grad, float* mo
                                                 const fc_segments* segs, fc_world* world,
                                                 void* stream);
 
+/* ------------------------------------------------ bf16 gradient wire format
+ * SURVEY §8 f4 (16-bit gradients on the wire).  `grad` holds n
+ * bfloat16 values (uint16 bit patterns; for the collective: symmetric in the
+ * heap), w and mom fp32.  Each gradient is upcast EXACTLY to fp32 and the rest
+ * is the fp32 path: the same tree association (R1), the same SGD
+ * (R6, with segs' multipliers if segs != NULL), fp32 weights broadcast.  So the
+ * result equals firecaffe_tree_allreduce_sgd applied to the upcast gradients,
+ * bit for bit; the reduce phase moves 2 instead of 4 bytes per parameter.
+ * The collective always uses the FLAT executor (the world's schedule is
+ * ignored); world_size 1 = firecaffe_sgd_step_bf16.  grad is read-only.
+ * Errors as firecaffe_tree_allreduce_sgd. */
+fc_status firecaffe_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int64_t n, float lr,
+                                  float mu, float wd, int64_t batch, const fc_segments* segs,
+                                  void* stream);
+fc_status firecaffe_tree_allreduce_sgd_bf16(float* w, uint16_t* grad, float* mom, int64_t n,
+                                            float lr, float mu, float wd, int64_t batch,
+                                            const fc_segments* segs, fc_world* world,
+                                            void* stream);
+
 /* ------------------------------------------------ host-buffer entry points
  * The same operations fed from / returned to HOST memory, for callers whose
  * gradients live on the host (and for the end-to-end benchmark).  grad_host

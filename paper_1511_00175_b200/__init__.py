@@ -143,6 +143,31 @@ def firecaffe_tree_allreduce_sgd_segments(w, grad, mom, lr, mu, wd, batch, segs:
           "firecaffe_tree_allreduce_sgd_segments")
 
 
+def _bptr(x) -> int:
+    """Device pointer of a bf16 gradient tensor."""
+    if isinstance(x, int):
+        return x
+    import torch
+
+    if not x.is_cuda or not x.is_contiguous() or x.dtype not in (torch.bfloat16, torch.int16, torch.uint16):
+        raise ValueError("bf16 gradients must be contiguous CUDA bfloat16 tensors")
+    return x.data_ptr()
+
+
+def firecaffe_sgd_step_bf16(w, grad_bf16, mom, lr, mu, wd, batch, segs=None, n=None, stream=None):
+    """firecaffe_sgd_step with a bf16 gradient (exact upcast)."""
+    check(load().firecaffe_sgd_step_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w), lr, mu, wd, int(batch),
+                                         segs.handle if segs else None, _stream(stream)), "firecaffe_sgd_step_bf16")
+
+
+def firecaffe_tree_allreduce_sgd_bf16(w, grad_bf16, mom, lr, mu, wd, batch, world: "World", segs=None, n=None,
+                                      stream=None):
+    """The fused tree allreduce + SGD with bf16 gradients on the wire."""
+    check(load().firecaffe_tree_allreduce_sgd_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w), lr, mu, wd,
+                                                   int(batch), segs.handle if segs else None, world.handle,
+                                                   _stream(stream)), "firecaffe_tree_allreduce_sgd_bf16")
+
+
 def _hptr(x) -> int:
     if isinstance(x, int):
         return x

@@ -62,6 +62,8 @@ SIGNATURES = {
     "firecaffe_sgd_step_segments": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
     "firecaffe_tree_allreduce_sgd_segments": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
     "firecaffe_lr_at": (_F, [_P, _I64]),
+    "firecaffe_sgd_step_bf16": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
+    "firecaffe_tree_allreduce_sgd_bf16": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
     "firecaffe_sgd_step_host": (_I, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
     "firecaffe_tree_allreduce_sgd_host": (_I, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
 }

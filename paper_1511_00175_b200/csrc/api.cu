@@ -370,12 +370,14 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     if (cur != w->device) return FC_ERR_MISMATCH;
     FcColl c;
     memset(&c, 0, sizeof(c));
-    c.off_grad = heap_offset(w, grad, n);
+    const bool bf16 = op == FC_OP_ALLREDUCE_SGD_BF16;
+    // (bf16 gradients: half the bytes; heap_offset checks n*4, which covers them)
+    c.off_grad = heap_offset(w, grad, bf16 ? (n + 1) / 2 : n);
     if (c.off_grad < 0) return FC_ERR_NOT_SYMMETRIC;
     c.off_w = 0;
     c.off_mom = -1;
     uint32_t seg_hash = 0;
-    if (op == FC_OP_ALLREDUCE_SGD) {
+    if (op == FC_OP_ALLREDUCE_SGD || bf16) {
         c.off_w = heap_offset(w, wt, n);
         if (c.off_w < 0) return FC_ERR_NOT_SYMMETRIC;
         if (w->virt) {
@@ -424,8 +426,8 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.bar_words = w->layout.bar_words;
     c.red_words = w->layout.red_words;
     c.max_chunks = w->layout.max_chunks;
-    const int sched = op == FC_OP_PS ? FC_SCHED_FLAT : w->sched;
-    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op == FC_OP_PS, n);
+    const int sched = (op == FC_OP_PS || bf16) ? FC_SCHED_FLAT : w->sched;
+    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op, n);
     if (grid < 1) return FC_ERR_UNSUPPORTED;
     w->last_grid = grid;
     const int64_t need = (int64_t)grid * (w->virt ? w->p : 1) * FC_TRACE_SLOTS;
@@ -480,6 +482,48 @@ fc_status firecaffe_tree_allreduce_sgd_segments(float* wt, float* grad, float* m
                                                 void* stream) {
     if (!segs) return FC_ERR_INVALID_ARG;
     return fused_impl(wt, grad, mom, n, lr, mu, wd, batch, segs, w, stream);
+}
+
+static bool overlap2(const void* a, int64_t abytes, const void* b, int64_t bbytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + (uintptr_t)bbytes && y < x + (uintptr_t)abytes;
+}
+
+static fc_status check_bf16_args(float* wt, const uint16_t* grad, float* mom, int64_t n, float lr,
+                                 float mu, float wd, int64_t batch) {
+    if (n < 0) return FC_ERR_INVALID_ARG;
+    fc_status st = check_hyper(lr, mu, wd, batch);
+    if (st != FC_OK) return st;
+    if (n == 0) return FC_OK;
+    if (check_vec(wt, n) || check_vec(grad, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    if (overlap2(wt, 4 * n, grad, 2 * n) || overlap2(wt, 4 * n, mom, 4 * n) ||
+        overlap2(grad, 2 * n, mom, 4 * n))
+        return FC_ERR_INVALID_ARG;
+    return FC_OK;
+}
+
+fc_status firecaffe_sgd_step_bf16(float* wt, const uint16_t* grad, float* mom, int64_t n, float lr,
+                                  float mu, float wd, int64_t batch, const fc_segments* segs,
+                                  void* stream) {
+    fc_status st = check_bf16_args(wt, grad, mom, n, lr, mu, wd, batch);
+    if (st != FC_OK || n == 0) return st;
+    FcSegs sd;
+    st = check_segs(segs, n, &sd);
+    if (st != FC_OK) return st;
+    cudaError_t e = launch_sgd_step_bf16(wt, grad, mom, n, lr, mu, wd, inv_batch(batch), sd,
+                                         (cudaStream_t)stream);
+    return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
+}
+
+fc_status firecaffe_tree_allreduce_sgd_bf16(float* wt, uint16_t* grad, float* mom, int64_t n,
+                                            float lr, float mu, float wd, int64_t batch,
+                                            const fc_segments* segs, fc_world* w, void* stream) {
+    if (!w) return FC_ERR_INVALID_ARG;
+    fc_status st = check_bf16_args(wt, grad, mom, n, lr, mu, wd, batch);
+    if (st != FC_OK || n == 0) return st;
+    if (w->p == 1) return firecaffe_sgd_step_bf16(wt, grad, mom, n, lr, mu, wd, batch, segs, stream);
+    return collective(w, FC_OP_ALLREDUCE_SGD_BF16, wt, (float*)grad, mom, n, lr, mu, wd, batch, segs,
+                      stream);
 }
 
 fc_status firecaffe_segments_create(const fc_segment* segs, int nseg, int64_t n,

@@ -70,4 +70,4 @@ struct FcColl {
 
 #define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit
 
-enum FcOp { FC_OP_ALLREDUCE = 0, FC_OP_ALLREDUCE_SGD = 1, FC_OP_PS = 2 };
+enum FcOp { FC_OP_ALLREDUCE = 0, FC_OP_ALLREDUCE_SGD = 1, FC_OP_PS = 2, FC_OP_ALLREDUCE_SGD_BF16 = 3 };

@@ -19,6 +19,9 @@ cudaError_t launch_sgd_step_range(float* w, const float* grad, float* mom, int64
                                   float lr, float mu, float wd, float inv_b, const FcSegs& segs,
                                   cudaStream_t st);
 void set_sgd_unroll(int u);
+cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int64_t n, float lr,
+                                 float mu, float wd, float inv_b, const FcSegs& segs,
+                                 cudaStream_t st);
 
 // Host-buffer pipeline (host_pipeline.cu)
 constexpr int kPipeDepth = 4;
@@ -31,7 +34,7 @@ cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_d
 cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
                               cudaStream_t st);
 // Max CTAs per rank that can be co-resident for this schedule (virt: divided by p).
-int collective_grid(int sched, int arity, int p, bool virt, bool ps, int64_t n);
+int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n);
 
 // Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
 __host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }

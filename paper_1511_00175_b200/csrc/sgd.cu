@@ -53,6 +53,75 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
     }
 }
 
+// bf16-gradient variant: grad holds bf16 (upcast exactly to fp32),
+// w and mom fp32; 4 elements per unit (8 B of gradient, 16 B of w and of mom),
+// every access coalesced; U units per thread in flight.
+template <int U>
+__global__ void __launch_bounds__(256) sgd_step_bf16_kernel(float4* __restrict__ w4,
+                                                            const uint2* __restrict__ g4,
+                                                            float4* __restrict__ v4, int64_t n4,
+                                                            int64_t n, float lr, float mu, float wd,
+                                                            float inv_b, const FcSegs segs) {
+    const int64_t T = blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    for (int64_t b0 = (int64_t)blockIdx.x * T * U + threadIdx.x; b0 < n4; b0 += stride) {
+        uint2 g[U];
+        float4 w[U], v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = b0 + j * T;
+            if (i < n4) {
+                asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];"
+                             : "=r"(g[j].x), "=r"(g[j].y)
+                             : "l"(g4 + i));
+                w[j] = ld_rw(w4 + i);
+                v[j] = ld_rw(v4 + i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = b0 + j * T;
+            if (i < n4) {
+                const float4 S = make_float4(__uint_as_float(g[j].x << 16), __uint_as_float(g[j].x & 0xffff0000u),
+                                             __uint_as_float(g[j].y << 16), __uint_as_float(g[j].y & 0xffff0000u));
+                sgd4_any(segs, 4 * i, S, w[j], v[j], lr, mu, wd, inv_b);
+                st_na(w4 + i, w[j]);
+                st_na(v4 + i, v[j]);
+            }
+        }
+    }
+    // the n % 4 trailing elements
+    const int tail = (int)(n - 4 * n4);
+    if (blockIdx.x == gridDim.x - 1 && (int)threadIdx.x < tail) {
+        const int64_t e = 4 * n4 + threadIdx.x;
+        float* wf = reinterpret_cast<float*>(w4);
+        float* vf = reinterpret_cast<float*>(v4);
+        const uint16_t h = reinterpret_cast<const uint16_t*>(g4)[e];
+        float ww = wf[e], vv = vf[e];
+        sgd1_any(segs, e, __uint_as_float((uint32_t)h << 16), ww, vv, lr, mu, wd, inv_b);
+        wf[e] = ww;
+        vf[e] = vv;
+    }
+}
+
+cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int64_t n, float lr,
+                                 float mu, float wd, float inv_b, const FcSegs& segs,
+                                 cudaStream_t st) {
+    constexpr int U = 4, T = 256;
+    const int64_t n4 = n / 4;
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sgd_step_bf16_kernel<U>, T, 0);
+    if (e != cudaSuccess) return e;
+    int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
+    int64_t cap = (int64_t)dev_info().sms * (occ > 0 ? occ : 1);
+    int64_t grid = want < cap ? want : cap;
+    if (grid < 1) grid = 1;
+    sgd_step_bf16_kernel<U><<<(unsigned)grid, T, 0, st>>>((float4*)w, (const uint2*)grad,
+                                                          (float4*)mom, n4, n, lr, mu, wd, inv_b,
+                                                          segs);
+    return cudaGetLastError();
+}
+
 static int g_sgd_unroll = 4;
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,

@@ -276,6 +276,103 @@ __device__ __forceinline__ void copy_chunk(const FcColl& c, int64_t cc, const fl
     }
 }
 
+// ------------------------------------------------------------ FLAT, bf16 wire
+// SURVEY §8 f4 (16-bit gradients on the wire).  Every rank's
+// gradient is bf16; the owner upcasts each operand exactly to fp32 and then
+// evaluates the same K-nomial tree in fp32 (R22), applies SGD in
+// fp32 and pushes fp32 weights.  The reduce phase moves half the bytes.
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
+__device__ __forceinline__ const uint16_t* gradh_of(const FcColl& c, int q) {
+    return reinterpret_cast<const uint16_t*>(c.peers.heap[q] + c.off_grad);
+}
+
+// 4 elements per unit: 8-byte bf16 loads and float4 weight accesses are both
+// fully coalesced per warp; U units per thread keep (P-1)*8*U remote bytes in
+// flight per thread.
+#define BF16_UNROLL(P) ((P) <= 2 ? 8 : (P) <= 4 ? 4 : 1)
+__device__ __forceinline__ uint2 ld_cg_u2(const uint2* p) {
+    uint2 r;
+    asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float4 bf16x4_to_f32(const uint2 u) {
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
+
+template <int P, int K>
+__global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
+    constexpr int U = BF16_UNROLL(P);
+    const int rank = my_rank(c);
+    trace(c, 0);
+    const bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
+    if (ok) {
+        const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+        int64_t c0, c1;
+        owned_chunks(rank, P, nch, false, &c0, &c1);
+        const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+        const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+        if (e1 > e0) {
+            const int64_t i0 = e0 / 4, i1 = e1 / 4;  // units of 4 elements (8 B of bf16)
+            float4* w4 = reinterpret_cast<float4*>(w_of(c, rank));
+            float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
+            const int64_t T = FLAT_T;
+            const int64_t stride = (int64_t)gridDim.x * T * U;
+            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < i1; base += stride) {
+                uint2 x[U][P];
+                float4 w[U], v[U];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int64_t i = base + j * T;
+                    if (i < i1) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            x[j][q] = ld_cg_u2(reinterpret_cast<const uint2*>(gradh_of(c, q)) + i);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int64_t i = base + j * T;
+                    if (i < i1) {
+                        w[j] = ld_rw(w4 + i);
+                        v[j] = ld_rw(v4 + i);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int64_t i = base + j * T;
+                    if (i < i1) {
+                        float4 f[P];
+#pragma unroll
+                        for (int q = 0; q < P; ++q) f[q] = bf16x4_to_f32(x[j][q]);
+                        const float4 S = tree_sum_regs<P, K>(f);
+                        sgd4_any(c.segs, 4 * i, S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                        st_na(v4 + i, v[j]);
+#pragma unroll
+                        for (int q = 0; q < P; ++q) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
+                    }
+                }
+            }
+            const int rem = (int)(e1 - 4 * i1);  // trailing n % 4 elements of the last slice
+            if (blockIdx.x == 0 && (int)threadIdx.x < rem) {
+                const int64_t e = 4 * i1 + threadIdx.x;
+                float xs[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) xs[q] = bf16_to_f32(gradh_of(c, q)[e]);
+                const float S = tree_sum_regs1<P, K>(xs);
+                float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
+                sgd1_any(c.segs, e, S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                st1(mom_of(c, rank) + e, vv);
+                for (int q = 0; q < P; ++q) st1(w_of(c, q) + e, ww);
+            }
+        }
+    }
+    trace(c, 2);
+    cta_barrier(c, rank, 1);
+    trace(c, 3);
+}
+
 // ------------------------------------------------------------ FLAT / PS ----
 // One communication level: the owner of slice [e0, e1) loads all P ranks'
 // values, evaluates the K-nomial tree in registers (K = P: the parameter
@@ -568,6 +665,18 @@ static const void* flat_for(int K) {
 }
 
 template <int P>
+static const void* bf16_for(int K) {
+    if (K >= P) K = P;
+    switch (K) {
+        case 2: return (const void*)flat_bf16_kernel<P, 2>;
+#define FC_K(k) case k: if constexpr (P >= k) return (const void*)flat_bf16_kernel<P, k>; else return nullptr;
+        FC_K(3) FC_K(4) FC_K(5) FC_K(6) FC_K(7) FC_K(8)
+#undef FC_K
+    }
+    return nullptr;
+}
+
+template <int P>
 static const void* forest_for() {
     if constexpr ((P & (P - 1)) == 0) return (const void*)forest_kernel<P>;
     else return nullptr;
@@ -581,12 +690,14 @@ struct KernelPick {
 
 static KernelPick pick_kernel(int sched, int arity, int p, int op) {
     if (op == FC_OP_PS) arity = p;
-    const bool flat = op == FC_OP_PS || sched == FC_SCHED_FLAT;
+    const bool bf16 = op == FC_OP_ALLREDUCE_SGD_BF16;  // always the FLAT executor
+    const bool flat = op == FC_OP_PS || sched == FC_SCHED_FLAT || bf16;
     KernelPick k{nullptr, flat ? FLAT_T : TREE_T, flat};
     switch (p) {
 #define FC_P(PP)                                                                              \
     case PP:                                                                                  \
-        if (flat) k.fn = flat_for<PP>(arity);                                                 \
+        if (bf16) k.fn = bf16_for<PP>(arity);                                                 \
+        else if (flat) k.fn = flat_for<PP>(arity);                                            \
         else if (sched == FC_SCHED_SINGLE_ROOT) k.fn = (const void*)single_root_kernel<PP>;   \
         else k.fn = forest_for<PP>();                                                         \
         break;
@@ -601,8 +712,8 @@ static KernelPick pick_kernel(int sched, int arity, int p, int op) {
 // of CTAs issuing it (4.4 us at 148 CTAs, 7.8 us at 444; scripts/fence_bench.cu,
 // launch_bench.cu).  Tree schedules: as many 256-thread CTAs as fit (their
 // chunk pipeline wants more independent CTAs).  Virtual worlds share one GPU.
-int collective_grid(int sched, int arity, int p, bool virt, bool ps, int64_t n) {
-    const KernelPick k = pick_kernel(sched, arity, p, ps ? FC_OP_PS : FC_OP_ALLREDUCE);
+int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
+    const KernelPick k = pick_kernel(sched, arity, p, op);
     if (!k.fn || p < 1) return 0;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.block, 0) != cudaSuccess) return 0;

@@ -62,11 +62,11 @@ def exchange_handles(local: bytes, group=None) -> list:
     return out
 
 
-def _as_tensor(ptr: int, n: int, device_index: int):
+def _as_tensor(ptr: int, n: int, device_index: int, typestr: str = "<f4"):
     import torch
 
     class _Arr:
-        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+        __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
                                     "strides": None}
 
     return torch.as_tensor(_Arr(), device=torch.device("cuda", device_index))
@@ -137,13 +137,23 @@ class World:
         return self
 
     # -- buffers ----------------------------------------------------------------
-    def alloc(self, n: int):
-        """Carve n floats at a symmetric offset.  Returns the local tensor (real
-        world) or a list of p tensors, one per virtual rank (rank 0 first)."""
-        off = self.layout.alloc(4 * int(n))
+    def alloc(self, n: int, dtype: str = "f32"):
+        """Carve n elements (fp32, or bf16 with dtype="bf16") at a symmetric offset.
+        Returns the local tensor (real world) or a list of p tensors, one per
+        virtual rank (rank 0 first)."""
+        esz = 2 if dtype == "bf16" else 4
+        off = self.layout.alloc(esz * int(n))
+
+        def view(ptr):
+            if dtype == "bf16":
+                import torch
+
+                return _as_tensor(ptr, int(n), self.device, "<i2").view(torch.bfloat16)
+            return _as_tensor(ptr, int(n), self.device)
+
         if self.virt:
-            return [_as_tensor(self.heap + r * self.heap_bytes + off, int(n), self.device) for r in range(self.p)]
-        return _as_tensor(self.heap + off, int(n), self.device)
+            return [view(self.heap + r * self.heap_bytes + off) for r in range(self.p)]
+        return view(self.heap + off)
 
     # -- configuration ------------------------------------------------------------
     def config(self, sched="forest", bcast="direct", arity: int = 2):

@@ -362,6 +362,48 @@ def test_sgd_step_host_pipeline_bitexact(n, with_segs):
         fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g, w_host, **HYPER)
 
 
+@pytest.mark.parametrize("n", [7, 4105, 100_003])
+@pytest.mark.parametrize("with_segs", [False, True])
+def test_sgd_step_bf16_bitexact(n, with_segs):
+    """bf16 gradients (reading R22): exact upcast, then the fp32 rule."""
+    g_bf = fc_inputs.grad(n, 0, seed=n + 5, dist="mixed").to(torch.bfloat16)
+    up = g_bf.float().numpy()
+    w, v = fc_inputs.weights(n, seed=6), fc_inputs.momentum(n, seed=7)
+    wd_, vd = w.cuda(), v.cuda()
+    segs = None
+    if with_segs:
+        b, lm, dm = fc_inputs.caffe_blobs(n)
+        segs = fc.Segments(b, lm, dm, n)
+        w_ref, v_ref = oracle.sgd_segments(w.numpy(), v.numpy(), up, **HYPER, begins=b, lr_mults=lm, decay_mults=dm)
+    else:
+        w_ref, v_ref = oracle.sgd(w.numpy(), v.numpy(), up, **HYPER)
+    fc.firecaffe_sgd_step_bf16(wd_, g_bf.cuda(), vd, **HYPER, segs=segs)
+    assert_bitexact(wd_, w_ref, "w")
+    assert_bitexact(vd, v_ref, "v")
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("n", [9, 4096 * 3 + 5, 100_003])
+def test_virtual_fused_bf16_bitexact(p, n):
+    W = _world(p, n)
+    try:
+        gb, ws, moms = W.alloc(n, "bf16"), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=7000 + p + n, dist="mixed").to(torch.bfloat16)
+        w0, v0 = fc_inputs.weights(n, seed=3), fc_inputs.momentum(n, seed=4)
+        _fill(gb, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd_bf16(ws[0], gb[0], moms[0], world=W, n=n, **HYPER)
+        assert W.poll() == 0
+        w_ref, v_ref = oracle.fused_step(g.float().numpy(), w0.numpy(), v0.numpy(), **HYPER)
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            assert_bitexact(moms[r][b:e], v_ref[b:e], f"mom rank {r}")
+    finally:
+        W.close()
+
+
 def test_sgd_step_vgg19_full_size_every_element():
     """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
     cfg = fc_inputs.CONFIGS["vgg19"]
