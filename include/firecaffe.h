@@ -31,6 +31,9 @@
  *     MPI/NCCL convention).  Their `grad`, `w` (and, for a virtual world,
  *     `mom`) must lie inside the world's heap at the SAME byte offset on every
  *     rank (symmetric allocation), at or after firecaffe_heap_reserved_bytes().
+ *   - Every device-side call (all but the *_host entry points' host checks) can
+ *     be captured in a CUDA graph and replayed: kernel arguments do not change
+ *     between calls (the collectives' call counter lives in device memory).
  *   - Numerics: round-to-nearest-even fp32, no FTZ, no fast-math; the summation
  *     association is fixed (documented per call) so results are bitwise
  *     deterministic and identical on every rank.  Inputs must be

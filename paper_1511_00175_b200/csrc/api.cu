@@ -32,7 +32,7 @@ struct fc_world {
     int64_t heap_bytes;    // per rank
     char* peer[FC_MAX_RANKS];
     bool opened[FC_MAX_RANKS];
-    uint32_t epoch;
+    uint32_t* d_ctl;  // device call counter (graph-capturable epochs)
     uint64_t timeout_ns;
     int* d_status;
     int arity;
@@ -157,12 +157,13 @@ static fc_status world_common(fc_world* w, int world_size, int dev, int64_t heap
     w->p = world_size;
     w->device = dev;
     w->heap_bytes = heap_bytes;
-    w->epoch = 0;
     w->timeout_ns = timeout_ns ? timeout_ns : 30ull * 1000000000ull;
     w->layout = fc_flag_layout(heap_bytes);
     if (w->layout.total_bytes >= heap_bytes) return FC_ERR_INVALID_ARG;
     if (cudaMalloc(&w->d_status, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
     if (cudaMemset(w->d_status, 0, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMalloc(&w->d_ctl, 2 * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMemset(w->d_ctl, 0, 2 * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
     default_config(w);
     return FC_OK;
 }
@@ -240,6 +241,7 @@ fc_status firecaffe_world_destroy(fc_world* w) {
     for (int q = 0; q < FC_MAX_RANKS; ++q)
         if (w->opened[q] && cudaIpcCloseMemHandle(w->peer[q]) != cudaSuccess) st = FC_ERR_CUDA;
     if (w->d_status) cudaFree(w->d_status);
+    if (w->d_ctl) cudaFree(w->d_ctl);
     delete w;
     return st;
 }
@@ -396,7 +398,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     for (int q = 0; q < w->p; ++q) c.peers.heap[q] = w->peer[q];
     c.rank = w->virt ? -1 : w->rank;
     c.p = w->p;
-    c.epoch = ++w->epoch;
+    c.ctl = w->d_ctl;
     {  // call signature (FNV-1a): every rank must make the same call
         uint32_t h = 2166136261u;
         auto mix = [&h](const void* p, size_t len) {
@@ -435,7 +437,6 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     cudaError_t e = launch_collective(c, sched, w->arity, w->virt != 0, grid, (cudaStream_t)stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        --w->epoch;
         return FC_ERR_CUDA;
     }
     return FC_OK;

@@ -51,7 +51,7 @@ struct FcColl {
     FcPeers peers;
     int rank;          // >= 0: this process's rank; -1: virtual world, rank = blockIdx.y
     int p;             // world size
-    uint32_t epoch;    // call counter (same on every rank)
+    uint32_t* ctl;     // device call counter: [0] last completed epoch, [1] CTAs done
     uint32_t sig;      // hash of (op, n, schedule, hyper-parameters): must match on every rank
     int op;            // FcOp
     uint64_t timeout_ns;

@@ -73,6 +73,34 @@ __device__ __forceinline__ void trace(const FcColl& c, int slot) {
         c.trace[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * FC_TRACE_SLOTS + slot] = globaltimer();
 }
 
+// ------------------------------------------------------------ epochs -------
+// The call counter lives in device memory (c.ctl[0] = epoch of the last
+// completed call, c.ctl[1] = CTAs finished in the current call), so a call's
+// kernel arguments never change from call to call and the collectives can be
+// captured in a CUDA graph and replayed.  Every CTA reads the epoch at entry;
+// the last CTA to finish publishes the next one (stream order makes it visible
+// to the next launch).  All ranks make the same calls, so the counters agree.
+__shared__ uint32_t s_epoch;
+
+__device__ __forceinline__ void epoch_begin(const FcColl& c) {
+    if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)c.ctl + 1u;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void epoch_end(const FcColl& c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * gridDim.y;
+        const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
+        if (done == total) {
+            c.ctl[1] = 0u;
+            __threadfence();
+            atomicExch(c.ctl, s_epoch);
+        }
+    }
+}
+
 // ------------------------------------------------------------ sync ---------
 // All-to-all barrier among the CTAs with this blockIdx.x on every rank
 // (slot 0 = entry, 1 = exit).  Thread q < p pushes "rank arrived" into rank q's
@@ -92,18 +120,18 @@ __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
     const int t = threadIdx.x;
     bool good = true;
     if (t < c.p && t != rank) {
-        const uint64_t stamp = (uint64_t)c.epoch | ((uint64_t)c.sig << 32);
+        const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
         uint64_t* dst = bar_flag(c, t, slot, blockIdx.x, rank);
         if (slot == 0) st_relaxed_sys64(dst, stamp);
         else st_release_sys64(dst, stamp);
         const uint64_t* f = bar_flag(c, rank, slot, blockIdx.x, t);
         uint64_t v = ld_acquire_sys64(f);
-        if (!reached((uint32_t)v, c.epoch)) {
+        if (!reached((uint32_t)v, s_epoch)) {
             const uint64_t t0 = globaltimer();
             uint32_t spins = 0;
             while (true) {
                 v = ld_relaxed_sys64(f);
-                if (reached((uint32_t)v, c.epoch)) {
+                if (reached((uint32_t)v, s_epoch)) {
                     v = ld_acquire_sys64(f);
                     break;
                 }
@@ -117,7 +145,7 @@ __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
                 }
             }
         }
-        if (good && (uint32_t)v == c.epoch && (uint32_t)(v >> 32) != c.sig) {
+        if (good && (uint32_t)v == s_epoch && (uint32_t)(v >> 32) != c.sig) {
             atomicCAS(c.status, FC_OK, FC_ERR_MISMATCH);
             good = false;
         }
@@ -128,7 +156,7 @@ __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
 // One thread waits for a flag; the CTA learns the outcome.
 __device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
     bool good = true;
-    if (threadIdx.x == 0) good = wait_flag(f, c.epoch, c.timeout_ns, c.status);
+    if (threadIdx.x == 0) good = wait_flag(f, s_epoch, c.timeout_ns, c.status);
     return __syncthreads_and(good) != 0;
 }
 
@@ -304,6 +332,7 @@ template <int P, int K>
 __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
     constexpr int U = BF16_UNROLL(P);
     const int rank = my_rank(c);
+    epoch_begin(c);
     trace(c, 0);
     const bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
@@ -371,6 +400,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
     trace(c, 2);
     cta_barrier(c, rank, 1);
     trace(c, 3);
+    epoch_end(c);
 }
 
 // ------------------------------------------------------------ FLAT / PS ----
@@ -381,6 +411,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
 template <int P, int K, int U>
 __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     const int rank = my_rank(c);
+    epoch_begin(c);
     trace(c, 0);
     const bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
@@ -470,6 +501,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     trace(c, 2);
     cta_barrier(c, rank, 1);
     trace(c, 3);
+    epoch_end(c);
 }
 
 // ------------------------------------------------------------ FOREST -------
@@ -483,6 +515,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
     const bool direct = c.bcast == FC_BCAST_DIRECT;
     float* own = grad_of(c, rank);
+    epoch_begin(c);
     trace(c, 0);
     bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
@@ -499,7 +532,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
         const float* pg = grad_of(c, partner);
         const int next_partner = rank ^ (1 << (l + 1));
         auto stamp = [&](int64_t cx) {  // next-level consumer of chunk cx is the partner
-            if ((cx < mid_next) != keep_lower_next) st_relaxed_sys(red_flag(c, next_partner, l, cx), c.epoch);
+            if ((cx < mid_next) != keep_lower_next) st_relaxed_sys(red_flag(c, next_partner, l, cx), s_epoch);
         };
         int pend = 0;
         int64_t cc_last = -1;
@@ -528,7 +561,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
                 if ((rank >> i) & 1) rlo = m2; else rhi = m2;
             }
             float* dst = fused ? w_of(c, partner) : grad_of(c, partner);
-            auto stamp = [&](int64_t cx) { st_relaxed_sys(av_flag(c, partner, cx), c.epoch); };
+            auto stamp = [&](int64_t cx) { st_relaxed_sys(av_flag(c, partner, cx), s_epoch); };
             int pend = 0;
             int64_t cc_last = -1;
             for (int64_t cc = first_chunk(rlo, G, b); cc < rhi; cc += G) {
@@ -551,6 +584,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
         cta_barrier(c, rank, 1);
     }
     trace(c, 3);
+    epoch_end(c);
 }
 
 // ------------------------------------------------------------ SINGLE ROOT --
@@ -564,6 +598,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
     const bool direct = c.bcast == FC_BCAST_DIRECT;
     float* own = grad_of(c, rank);
+    epoch_begin(c);
     trace(c, 0);
     bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
@@ -586,7 +621,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         const bool root_final = (rank == 0) && (l == L - 1);
         const bool signal_parent = (l == last_recv) && (parent >= 0);
         const float* cg = grad_of(c, child);
-        auto stamp = [&](int64_t cx) { st_relaxed_sys(red_flag(c, parent, send_level, cx), c.epoch); };
+        auto stamp = [&](int64_t cx) { st_relaxed_sys(red_flag(c, parent, send_level, cx), s_epoch); };
         int pend = 0;
         int64_t cc_last = -1;
         for (int64_t cc = b; cc < nch; cc += G) {
@@ -611,7 +646,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
             if (rank + (1 << l) < P) dst[nd++] = fused ? w_of(c, rank + (1 << l)) : grad_of(c, rank + (1 << l));
         auto stamp = [&](int64_t cx) {
             for (int l = top - 1; l >= 0; --l)
-                if (rank + (1 << l) < P) st_relaxed_sys(av_flag(c, rank + (1 << l), cx), c.epoch);
+                if (rank + (1 << l) < P) st_relaxed_sys(av_flag(c, rank + (1 << l), cx), s_epoch);
         };
         int pend = 0;
         int64_t cc_last = -1;
@@ -628,6 +663,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         cta_barrier(c, rank, 1);
     }
     trace(c, 3);
+    epoch_end(c);
 }
 
 // ------------------------------------------------------------ dispatch -----

@@ -404,6 +404,50 @@ def test_virtual_fused_bf16_bitexact(p, n):
         W.close()
 
 
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("single_root", "direct")])
+def test_cuda_graph_capture_and_replay(sched, bcast):
+    """The collectives keep their call counter on the device, so a captured step
+    replays correctly: 3 replays == 3 eager calls, bit for bit."""
+    p, n = 4, 3 * 4096 + 5
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=808)
+        w0, v0 = fc_inputs.weights(n, seed=809), fc_inputs.momentum(n, seed=810)
+
+        def reset():
+            _fill(grads, g)
+            _fill(ws, [w0] * p)
+            _fill(moms, [v0] * p)
+
+        reset()
+        for _ in range(3):
+            fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+            _fill(grads, g)  # single_root keeps partial sums in grad
+        eager_w = [x.clone() for x in ws]
+        eager_m = [x.clone() for x in moms]
+        reset()
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+        torch.cuda.current_stream().wait_stream(s)
+        reset()  # (capture does not execute)
+        for _ in range(3):
+            graph.replay()
+            torch.cuda.synchronize()
+            _fill(grads, g)
+        assert W.poll() == 0
+        for r in range(p):
+            assert torch.equal(ws[r], eager_w[r]), f"w rank {r}"
+            assert torch.equal(moms[r], eager_m[r]), f"mom rank {r}"
+    finally:
+        W.close()
+
+
 def test_sgd_step_vgg19_full_size_every_element():
     """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
     cfg = fc_inputs.CONFIGS["vgg19"]
