@@ -287,6 +287,14 @@ typedef struct {
 } fc_lr_schedule;
 float firecaffe_lr_at(const fc_lr_schedule* sched, int64_t iter);
 
+/* firecaffe_allgather_owned — every rank's firecaffe_owned_range slice of the
+ * symmetric buffer `buf` is copied to every other rank, in place: afterwards all
+ * ranks hold the owners' values everywhere.  Use it on the momentum before a
+ * checkpoint (firecaffe_tree_allreduce_sgd keeps it sharded, R18) or
+ * before changing the executor (ownership differs for FC_SCHED_SINGLE_ROOT).
+ * Collective; `buf` must be symmetric in the heap.  world_size 1: no-op. */
+fc_status firecaffe_allgather_owned(float* buf, int64_t n, fc_world* world, void* stream);
+
 /* Linear learning-rate scaling with the batch size:
  * returns fl(base_lr * batch / base_batch) computed in double, e.g. (0.01, 256, 1024) -> 0.04.
  * Returns 0 for base_batch < 1 or batch < 1. */

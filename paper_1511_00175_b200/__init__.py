@@ -75,6 +75,13 @@ def firecaffe_ps_allreduce(grad, world: "World", n=None, stream=None):
           "firecaffe_ps_allreduce")
 
 
+def firecaffe_allgather_owned(buf, world: "World", n=None, stream=None):
+    """Copy every rank's owned slice of a symmetric buffer to all ranks (checkpoint the
+    sharded momentum)."""
+    check(load().firecaffe_allgather_owned(_ptr(buf), _numel(n, buf), world.handle, _stream(stream)),
+          "firecaffe_allgather_owned")
+
+
 def firecaffe_scale_lr(base_lr: float, base_batch: int, batch: int) -> float:
     return load().firecaffe_scale_lr(base_lr, base_batch, batch)
 

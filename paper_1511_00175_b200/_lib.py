@@ -51,6 +51,7 @@ SIGNATURES = {
     "firecaffe_tree_allreduce": (_I, [_P, _I64, _P, _P]),
     "firecaffe_tree_allreduce_sgd": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
     "firecaffe_ps_allreduce": (_I, [_P, _I64, _P, _P]),
+    "firecaffe_allgather_owned": (_I, [_P, _I64, _P, _P]),
     "firecaffe_scale_lr": (_F, [_F, _I64, _I64]),
     "firecaffe_status_str": (ctypes.c_char_p, [_I]),
     "firecaffe_tune_sgd_unroll": (None, [_I]),

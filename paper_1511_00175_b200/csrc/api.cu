@@ -421,6 +421,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         c.sig = h;
     }
     c.op = op;
+    c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;
     c.n = n;
@@ -447,6 +448,13 @@ fc_status firecaffe_tree_allreduce(float* grad, int64_t n, fc_world* w, void* st
     if (n == 0 || w->p == 1) return FC_OK;
     if (check_vec(grad, n)) return FC_ERR_INVALID_ARG;
     return collective(w, FC_OP_ALLREDUCE, nullptr, grad, nullptr, n, 0, 0, 0, 1, nullptr, stream);
+}
+
+fc_status firecaffe_allgather_owned(float* buf, int64_t n, fc_world* w, void* stream) {
+    if (!w || n < 0) return FC_ERR_INVALID_ARG;
+    if (n == 0 || w->p == 1) return FC_OK;
+    if (check_vec(buf, n)) return FC_ERR_INVALID_ARG;
+    return collective(w, FC_OP_ALLGATHER_OWNED, nullptr, buf, nullptr, n, 0, 0, 0, 1, nullptr, stream);
 }
 
 fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* w, void* stream) {

@@ -64,10 +64,17 @@ struct FcColl {
     float lr, mu, wd, inv_b;
     FcSegs segs;       // per-blob multipliers for the fused update
     int bcast;         // fc_bcast
+    int owner_single_root;  // ownership of the single-root schedule (rank 0 owns all)
     int64_t bar_words, red_words, max_chunks;
     uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]
 };
 
 #define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit
 
-enum FcOp { FC_OP_ALLREDUCE = 0, FC_OP_ALLREDUCE_SGD = 1, FC_OP_PS = 2, FC_OP_ALLREDUCE_SGD_BF16 = 3 };
+enum FcOp {
+    FC_OP_ALLREDUCE = 0,
+    FC_OP_ALLREDUCE_SGD = 1,
+    FC_OP_PS = 2,
+    FC_OP_ALLREDUCE_SGD_BF16 = 3,
+    FC_OP_ALLGATHER_OWNED = 4
+};

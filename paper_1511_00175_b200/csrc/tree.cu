@@ -403,6 +403,59 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
     epoch_end(c);
 }
 
+// ------------------------------------------------------------ ALLGATHER ----
+// op FC_OP_ALLGATHER_OWNED: every rank pushes its owned slice of a symmetric
+// buffer (off_grad) to every other rank, so all ranks end with the full vector
+// (e.g. the sharded momentum of the fused update, for a checkpoint: R18).
+template <int P>
+__global__ void __launch_bounds__(FLAT_T) allgather_kernel(const FcColl c) {
+    const int rank = my_rank(c);
+    epoch_begin(c);
+    trace(c, 0);
+    const bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
+    if (ok) {
+        const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+        int64_t c0, c1;
+        owned_chunks(rank, P, nch, c.owner_single_root != 0, &c0, &c1);
+        const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+        const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+        if (e1 > e0) {
+            const int64_t i0 = e0 / 4, i1 = e1 / 4;
+            const float4* src = reinterpret_cast<const float4*>(grad_of(c, rank));
+            const int64_t stride = (int64_t)gridDim.x * FLAT_T * 2;
+            for (int64_t base = i0 + (int64_t)blockIdx.x * FLAT_T * 2 + threadIdx.x; base < i1; base += stride) {
+                float4 x[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int64_t i = base + j * FLAT_T;
+                    if (i < i1) x[j] = ld_cg(src + i);
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int64_t i = base + j * FLAT_T;
+                    if (i < i1) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            if (q != rank) st_na(reinterpret_cast<float4*>(grad_of(c, q)) + i, x[j]);
+                    }
+                }
+            }
+            const int rem = (int)(e1 - 4 * i1);
+            if (blockIdx.x == 0 && (int)threadIdx.x < rem) {
+                const int64_t e = 4 * i1 + threadIdx.x;
+                const float v = ld_cg1(grad_of(c, rank) + e);
+                for (int q = 0; q < P; ++q)
+                    if (q != rank) st1(grad_of(c, q) + e, v);
+            }
+        }
+    }
+    trace(c, 2);
+    cta_barrier(c, rank, 1);
+    trace(c, 3);
+    epoch_end(c);
+}
+
 // ------------------------------------------------------------ FLAT / PS ----
 // One communication level: the owner of slice [e0, e1) loads all P ranks'
 // values, evaluates the K-nomial tree in registers (K = P: the parameter
@@ -727,12 +780,14 @@ struct KernelPick {
 static KernelPick pick_kernel(int sched, int arity, int p, int op) {
     if (op == FC_OP_PS) arity = p;
     const bool bf16 = op == FC_OP_ALLREDUCE_SGD_BF16;  // always the FLAT executor
-    const bool flat = op == FC_OP_PS || sched == FC_SCHED_FLAT || bf16;
+    const bool gather = op == FC_OP_ALLGATHER_OWNED;
+    const bool flat = op == FC_OP_PS || sched == FC_SCHED_FLAT || bf16 || gather;
     KernelPick k{nullptr, flat ? FLAT_T : TREE_T, flat};
     switch (p) {
 #define FC_P(PP)                                                                              \
     case PP:                                                                                  \
-        if (bf16) k.fn = bf16_for<PP>(arity);                                                 \
+        if (gather) k.fn = (const void*)allgather_kernel<PP>;                                 \
+        else if (bf16) k.fn = bf16_for<PP>(arity);                                            \
         else if (flat) k.fn = flat_for<PP>(arity);                                            \
         else if (sched == FC_SCHED_SINGLE_ROOT) k.fn = (const void*)single_root_kernel<PP>;   \
         else k.fn = forest_for<PP>();                                                         \

@@ -448,6 +448,31 @@ def test_cuda_graph_capture_and_replay(sched, bcast):
         W.close()
 
 
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("sched", ["flat", "single_root"])
+def test_allgather_owned_momentum_checkpoint(p, sched):
+    """After the fused step mom is sharded (R18); allgather_owned reassembles the
+    oracle's full v' on every rank (checkpoint / executor change)."""
+    n = 4096 * p + 333
+    W = _world(p, n)
+    try:
+        W.config(sched, "direct", 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=900 + p)
+        w0, v0 = fc_inputs.weights(n, seed=901), fc_inputs.momentum(n, seed=902)
+        _fill(grads, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+        fc.firecaffe_allgather_owned(moms[0], W)
+        assert W.poll() == 0
+        _, v_ref = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **HYPER)
+        for r in range(p):
+            assert_bitexact(moms[r], v_ref, f"mom rank {r}")
+    finally:
+        W.close()
+
+
 def test_sgd_step_vgg19_full_size_every_element():
     """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
     cfg = fc_inputs.CONFIGS["vgg19"]
