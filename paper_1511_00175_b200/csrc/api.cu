@@ -594,6 +594,16 @@ fc_status firecaffe_segments_destroy(fc_segments* t) {
     return FC_OK;
 }
 
+// Device address of page-locked host memory (UVA-mapped), or null.
+static void* device_view(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
 static bool pinned_host(const void* p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -627,8 +637,22 @@ fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float
         chunk = (chunk + 3) / 4 * 4;
         if (chunk < 4096) chunk = 4096;
     }
-    cudaError_t e = launch_sgd_step_host(w, grad_host, grad, mom, w_host, n, lr, mu, wd,
-                                         inv_batch(batch), sd, chunk, (cudaStream_t)stream);
+    // zero-copy kernel (default) or copy-engine pipeline (FC_HOST_MODE=pipe)
+    static int mode = -1;
+    if (mode < 0) {
+        const char* m = getenv("FC_HOST_MODE");
+        mode = (m && strcmp(m, "pipe") == 0) ? 1 : 0;
+    }
+    cudaError_t e;
+    const float* gdev = (const float*)device_view(grad_host);
+    float* wdev = (float*)device_view(w_host);
+    if (mode == 0 && gdev && wdev && aligned16(gdev) && aligned16(wdev)) {
+        e = launch_sgd_step_hostio(w, gdev, grad, mom, wdev, n, lr, mu, wd, inv_batch(batch), sd,
+                                   (cudaStream_t)stream);
+    } else {
+        e = launch_sgd_step_host(w, grad_host, grad, mom, w_host, n, lr, mu, wd, inv_batch(batch), sd,
+                                 chunk, (cudaStream_t)stream);
+    }
     return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 

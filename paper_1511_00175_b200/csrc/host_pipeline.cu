@@ -6,10 +6,79 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "fc_internal.h"
+#include "fc_device.cuh"
 #include "fc_launch.h"
 
 namespace fc {
+
+// Zero-copy variant: ONE kernel reads the gradient straight from pinned host
+// memory over PCIe (UVA-mapped), keeps a device copy in `grad_dev`, applies the
+// SGD against w/mom in HBM and writes the new weights both to HBM and straight
+// back to pinned host memory.  PCIe reads (gradient) and posted writes
+// (weights) stream concurrently in both directions with no copy-engine stages
+// to fill or drain.
+template <int U>
+__global__ void __launch_bounds__(256) sgd_step_hostio_kernel(
+    float4* __restrict__ w4, const float4* __restrict__ gh4, float4* __restrict__ gd4,
+    float4* __restrict__ v4, float4* __restrict__ wh4, int64_t n4, int64_t n, float lr, float mu,
+    float wd, float inv_b, const FcSegs segs) {
+    const int64_t T = blockDim.x;
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    for (int64_t b0 = (int64_t)blockIdx.x * T * U + threadIdx.x; b0 < n4; b0 += stride) {
+        float4 g[U], w[U], v[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = b0 + j * T;
+            if (i < n4) {
+                g[j] = gh4[i];  // PCIe read of pinned host memory
+                w[j] = ld_rw(w4 + i);
+                v[j] = ld_rw(v4 + i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = b0 + j * T;
+            if (i < n4) {
+                st_na(gd4 + i, g[j]);
+                sgd4_any(segs, 4 * i, g[j], w[j], v[j], lr, mu, wd, inv_b);
+                st_na(w4 + i, w[j]);
+                st_na(v4 + i, v[j]);
+                wh4[i] = w[j];  // PCIe posted write to pinned host memory
+            }
+        }
+    }
+    const int tail = (int)(n - 4 * n4);
+    if (blockIdx.x == gridDim.x - 1 && (int)threadIdx.x < tail) {
+        const int64_t e = 4 * n4 + threadIdx.x;
+        const float gg = reinterpret_cast<const float*>(gh4)[e];
+        float* wf = reinterpret_cast<float*>(w4);
+        float* vf = reinterpret_cast<float*>(v4);
+        reinterpret_cast<float*>(gd4)[e] = gg;
+        float ww = wf[e], vv = vf[e];
+        sgd1_any(segs, e, gg, ww, vv, lr, mu, wd, inv_b);
+        wf[e] = ww;
+        vf[e] = vv;
+        reinterpret_cast<float*>(wh4)[e] = ww;
+    }
+}
+
+cudaError_t launch_sgd_step_hostio(float* w, const float* grad_host, float* grad_dev, float* mom,
+                                   float* w_host, int64_t n, float lr, float mu, float wd,
+                                   float inv_b, const FcSegs& segs, cudaStream_t st) {
+    constexpr int U = 4, T = 256;
+    const int64_t n4 = n / 4;
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sgd_step_hostio_kernel<U>, T, 0);
+    if (e != cudaSuccess) return e;
+    int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
+    int64_t cap = (int64_t)dev_info().sms * (occ > 0 ? occ : 1);
+    int64_t grid = want < cap ? want : cap;
+    if (grid < 1) grid = 1;
+    sgd_step_hostio_kernel<U><<<(unsigned)grid, T, 0, st>>>(
+        (float4*)w, (const float4*)grad_host, (float4*)grad_dev, (float4*)mom, (float4*)w_host, n4,
+        n, lr, mu, wd, inv_b, segs);
+    return cudaGetLastError();
+}
 
 struct PipeCtx {
     bool ready = false;
