@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <cmath>
+#include <mutex>
 
 #include "fc_internal.h"
 #include "fc_launch.h"
@@ -59,6 +60,29 @@ const DevInfo& dev_info() {
         have[d] = true;
     }
     return cache[d];
+}
+
+// Resident CTAs per SM of (kernel, block size) on the current device, cached:
+// the occupancy query costs microseconds and sits on every call's host path.
+int occupancy(const void* fn, int block) {
+    struct Entry {
+        const void* fn;
+        int block, device, occ;
+    };
+    static Entry table[512];
+    static int used = 0;
+    static std::mutex mu;
+    const int dev = dev_info().device;
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < used; ++i)
+        if (table[i].fn == fn && table[i].block == block && table[i].device == dev) return table[i].occ;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (used < 512) table[used++] = Entry{fn, block, dev, occ};
+    return occ;
 }
 }  // namespace fc
 

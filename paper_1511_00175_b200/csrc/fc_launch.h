@@ -12,6 +12,7 @@ struct DevInfo {
     int sms;
 };
 const DevInfo& dev_info();  // current device's SM count (cached per device)
+int occupancy(const void* fn, int block);  // resident CTAs/SM, cached per (kernel, block, device)
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
                             float wd, float inv_b, const FcSegs& segs, cudaStream_t st);

@@ -68,8 +68,7 @@ cudaError_t launch_sgd_step_hostio(float* w, const float* grad_host, float* grad
     constexpr int U = 4, T = 256;
     const int64_t n4 = n / 4;
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sgd_step_hostio_kernel<U>, T, 0);
-    if (e != cudaSuccess) return e;
+    occ = occupancy((const void*)sgd_step_hostio_kernel<U>, T);
     int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
     int64_t cap = (int64_t)dev_info().sms * (occ > 0 ? occ : 1);
     int64_t grid = want < cap ? want : cap;

@@ -110,8 +110,7 @@ cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int
     constexpr int U = 4, T = 256;
     const int64_t n4 = n / 4;
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sgd_step_bf16_kernel<U>, T, 0);
-    if (e != cudaSuccess) return e;
+    occ = occupancy((const void*)sgd_step_bf16_kernel<U>, T);
     int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
     int64_t cap = (int64_t)dev_info().sms * (occ > 0 ? occ : 1);
     int64_t grid = want < cap ? want : cap;
@@ -143,8 +142,7 @@ cudaError_t launch_sgd_step_range(float* w0, const float* grad0, float* mom0, in
     const DevInfo& di = dev_info();
     auto run = [&](auto kern, int U) -> cudaError_t {
         int occ = 0;
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, T, 0);
-        if (e != cudaSuccess) return e;
+        occ = occupancy((const void*)kern, T);
         int64_t want = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
         int64_t cap = (int64_t)di.sms * (occ > 0 ? occ : 1);
         int64_t grid = want < cap ? want : cap;

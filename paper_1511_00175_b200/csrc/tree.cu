@@ -807,7 +807,7 @@ int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
     const KernelPick k = pick_kernel(sched, arity, p, op);
     if (!k.fn || p < 1) return 0;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k.fn, k.block, 0) != cudaSuccess) return 0;
+    occ = occupancy(k.fn, k.block);
     if (occ < 1) return 0;
     static int flat_per_sm = -1;
     if (flat_per_sm < 0) {
@@ -824,7 +824,7 @@ int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
     int64_t cap = (int64_t)dev_info().sms * occ;
     if (virt) {
         int occ_all = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_all, k.fn, k.block, 0);
+        occ_all = occupancy(k.fn, k.block);
         cap = (int64_t)dev_info().sms * occ_all / p;
     }
     if (cap > FC_MAX_CTAS) cap = FC_MAX_CTAS;
