@@ -298,7 +298,7 @@ def main():
     fl_a = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     fl_b = torch.ones(512 << 18, dtype=torch.float32, device=dev)
 
-    def flush():
+    def flush_l2():
         if not args.no_flush:
             fl_a.zero_()
             fl_b.sum()
@@ -344,7 +344,11 @@ def main():
     parity = parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W)
 
     # ---- timed region
-    def timed(fn, K, Wm, pre=None):
+    def timed(fn, K, Wm, pre=None, cold=True):
+        def flush():
+            if cold:
+                flush_l2()
+
         for _ in range(Wm):
             if pre:
                 pre()
@@ -395,6 +399,9 @@ def main():
 
     reset()
     e2e_ms, _, _ = timed(e2e_step, max(5, min(args.steps, 50)), min(args.warmup, 5))
+    # secondary: warm L2 (no flush between steps), as in a loop whose working set stays resident
+    reset()
+    warm_ms, _, _ = timed(step, max(5, min(args.steps, 50)), min(args.warmup, 5), pre=restore, cold=False)
     e2e_value = N * 4 * n / (e2e_ms * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (the only kernel in the step)
@@ -493,10 +500,11 @@ def main():
             "ms_per_step_median": round(statistics.median(ms_list), 5),
             "roofline": roof,
             "cpu_baseline": cpu,
+            "ms_per_step_warm_l2": round(warm_ms, 5),
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_ms, 4),
-                    "what": ("firecaffe_sgd_step_host: pinned host grad -> device, SGD, updated w -> pinned "
-                             "host, chunk-pipelined (H2D || SGD || D2H)") if N == 1 else
+                    "what": ("firecaffe_sgd_step_host: one zero-copy kernel reads the pinned host grad over "
+                             "PCIe, updates w/mom in HBM, writes w to pinned host memory") if N == 1 else
                             "firecaffe_tree_allreduce_sgd_host: pinned host grad -> heap, fused tree, w -> host"},
             "gpu_launches": args.steps,
             "gpu_launches_note": "one library kernel per step (L2-flush and barrier kernels are torch/NCCL)",
@@ -545,6 +553,11 @@ def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, rese
     own = (idx >= b) & (idx < e)
     ok_v = bool(np.array_equal(mom[idx_d].cpu().numpy()[own.numpy()].view(np.uint32),
                                v_ref[own.numpy()].view(np.uint32)))
+    # north_star tolerance: vs a float64 left-to-right sum + float64 SGD (reading R15 scale)
+    w0s, v0s = w0[idx_d].cpu().numpy(), v0[idx_d].cpu().numpy()
+    w64, v64 = oracle.sgd_f64(w0s, v0s, oracle.sum_f64(G), **hp)
+    scale = np.abs(w0s).astype(np.float64) + np.abs(v64)
+    rel_f64 = float(np.max(np.abs(w_got.astype(np.float64) - w64) / np.maximum(scale, 1e-30)))
     digest = int(w.view(torch.int32).to(torch.int64).sum().item() % (1 << 61))
     ok = torch.tensor([1 if (ok_w and ok_v) else 0], device=grad.device)
     dg = torch.tensor([digest], dtype=torch.int64, device=grad.device)
@@ -557,7 +570,7 @@ def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, rese
         same = dmin.item() == dmax.item()
     status = W.poll() if W is not None else 0
     return {"bitexact_sampled": bool(ok.item() == 1), "samples": int(idx.numel()), "ranks_identical_digest": same,
-            "device_status": status}
+            "max_rel_err_w_vs_f64": rel_f64, "device_status": status}
 
 
 if __name__ == "__main__":
