@@ -187,11 +187,13 @@ __device__ __forceinline__ int64_t first_chunk(int64_t lo, int G, int b) {
 // lower rank group's partial plus the upper group's; fp32 addition commutes
 // bitwise, so operand order is immaterial).  Not last: s -> own grad (in
 // place).  Last (subtree root): fused -> SGD on w, mom; unfused -> s -> grad.
-// `direct`: also push the result to every other rank.
+// `push`: bitmask of ranks that also receive the result right away (last level
+// only): every other rank for a direct broadcast, the first broadcast hop for
+// a tree broadcast, so the root's link sends while it still receives.
 template <int P>
 __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t cc, float* own,
                                              const float* peer, bool last, bool fused,
-                                             bool direct) {
+                                             uint32_t push) {
     const int64_t e0 = cc * FC_CHUNK_FLOATS;
     const int64_t e1 = min(e0 + (int64_t)FC_CHUNK_FLOATS, c.n);
     const int nf4 = (int)((e1 - e0) >> 2);
@@ -215,10 +217,10 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
             if (k < nf4) {
                 const float4 s = add4(a[j], b[j]);
                 st_na(own4 + k, s);
-                if (last && direct) {
+                if (last && push) {
 #pragma unroll
                     for (int q = 0; q < P; ++q)
-                        if (q != rank) st_na(reinterpret_cast<float4*>(grad_of(c, q) + e0) + k, s);
+                        if ((push >> q) & 1u) st_na(reinterpret_cast<float4*>(grad_of(c, q) + e0) + k, s);
                 }
             }
         }
@@ -226,9 +228,9 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
             const int64_t e = e0 + 4 * (int64_t)nf4 + t;
             const float s = __fadd_rn(ld_cg1(own + e), ld_cg1(peer + e));
             st1(own + e, s);
-            if (last && direct)
+            if (last && push)
                 for (int q = 0; q < P; ++q)
-                    if (q != rank) st1(grad_of(c, q) + e, s);
+                    if ((push >> q) & 1u) st1(grad_of(c, q) + e, s);
         }
         return;
     }
@@ -252,10 +254,10 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
             sgd4_any(c.segs, e0 + 4 * (int64_t)k, s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
             st_na(w4 + k, w[j]);
             st_na(v4 + k, v[j]);
-            if (direct) {
+            if (push) {
 #pragma unroll
                 for (int q = 0; q < P; ++q)
-                    if (q != rank) st_na(reinterpret_cast<float4*>(w_of(c, q) + e0) + k, w[j]);
+                    if ((push >> q) & 1u) st_na(reinterpret_cast<float4*>(w_of(c, q) + e0) + k, w[j]);
             }
         }
     }
@@ -268,9 +270,9 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
         sgd1_any(c.segs, e, s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
         st1(wp, ww);
         st1(vp, vv);
-        if (direct)
+        if (push)
             for (int q = 0; q < P; ++q)
-                if (q != rank) st1(w_of(c, q) + e, ww);
+                if ((push >> q) & 1u) st1(w_of(c, q) + e, ww);
     }
 }
 
@@ -573,7 +575,12 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
 
-    // ---- reduce: recursive halving, level l pairs rank with rank ^ 2^l
+    // ---- reduce: recursive halving, level l pairs rank with rank ^ 2^l.  The
+    // last level also sends each finished chunk straight on: to every rank
+    // (direct) or to the first broadcast hop rank ^ 2^(M-1) (tree), so the
+    // owner's link sends while it still receives.
+    const uint32_t all_mask = ((1u << P) - 1u) & ~(1u << rank);
+    const int bc0 = rank ^ (1 << (M - 1));  // first hop of the tree broadcast
     int64_t lo = 0, hi = nch;
     for (int l = 0; l < M && ok; ++l) {
         const int partner = rank ^ (1 << l);
@@ -584,15 +591,21 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
         const bool keep_lower_next = ((rank >> (l + 1)) & 1) == 0;
         const float* pg = grad_of(c, partner);
         const int next_partner = rank ^ (1 << (l + 1));
-        auto stamp = [&](int64_t cx) {  // next-level consumer of chunk cx is the partner
-            if ((cx < mid_next) != keep_lower_next) st_relaxed_sys(red_flag(c, next_partner, l, cx), s_epoch);
+        const uint32_t push = !last ? 0u : (direct ? all_mask : (1u << bc0));
+        const bool publish = !last || !direct;
+        auto stamp = [&](int64_t cx) {
+            if (!last) {  // next-level consumer of chunk cx is the partner
+                if ((cx < mid_next) != keep_lower_next) st_relaxed_sys(red_flag(c, next_partner, l, cx), s_epoch);
+            } else {      // chunk cx of the owned slice has reached the first broadcast hop
+                st_relaxed_sys(av_flag(c, bc0, cx), s_epoch);
+            }
         };
         int pend = 0;
         int64_t cc_last = -1;
         for (int64_t cc = first_chunk(lo, G, b); cc < hi; cc += G) {
             if (l >= 1 && !wait_one(c, red_flag(c, rank, l - 1, cc))) { ok = false; break; }
-            reduce_chunk<P>(c, rank, cc, own, pg, last, fused, direct);
-            if (!last) {
+            reduce_chunk<P>(c, rank, cc, own, pg, last, fused, push);
+            if (publish) {
                 cc_last = cc;
                 if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
             }
@@ -605,7 +618,7 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
     if (!direct) {
         const int64_t o0 = lo, o1 = hi;  // owned slice
         float* mine = fused ? w_of(c, rank) : own;
-        for (int j = 0; j < M && ok; ++j) {
+        for (int j = 1; j < M && ok; ++j) {  // (level j = 0 was sent inside the last reduce level)
             const int l = M - 1 - j;
             const int partner = rank ^ (1 << l);
             int64_t rlo = 0, rhi = nch;  // region R_{l+1}(rank) held now
@@ -666,6 +679,12 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
     }
     const int parent = send_level >= 0 ? rank - (1 << send_level) : -1;
 
+    // The root's final level sends each finished chunk straight on: to every
+    // rank (direct) or to its children (tree), overlapping its send and receive.
+    uint32_t root_children = 0;
+    for (int l = 0; l < L; ++l)
+        if ((1 << l) < P) root_children |= 1u << (1 << l);
+    const uint32_t all_mask = ((1u << P) - 1u) & ~1u;
     for (int l = 0; l < L && ok; ++l) {
         if (rank % (2 << l) != 0) break;  // sent at an earlier level: done reducing
         const int child = rank + (1 << l);
@@ -673,14 +692,22 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
         const bool child_has_children = (l >= 1) && (child + 1 < P);
         const bool root_final = (rank == 0) && (l == L - 1);
         const bool signal_parent = (l == last_recv) && (parent >= 0);
+        const bool publish = signal_parent || (root_final && !direct);
+        const uint32_t push = root_final ? (direct ? all_mask : root_children) : 0u;
         const float* cg = grad_of(c, child);
-        auto stamp = [&](int64_t cx) { st_relaxed_sys(red_flag(c, parent, send_level, cx), s_epoch); };
+        auto stamp = [&](int64_t cx) {
+            if (signal_parent) {
+                st_relaxed_sys(red_flag(c, parent, send_level, cx), s_epoch);
+            } else {  // root, tree broadcast: the chunk has reached every child
+                for (int q = 1; q < P; q <<= 1) st_relaxed_sys(av_flag(c, q, cx), s_epoch);
+            }
+        };
         int pend = 0;
         int64_t cc_last = -1;
         for (int64_t cc = b; cc < nch; cc += G) {
             if (child_has_children && !wait_one(c, red_flag(c, rank, l, cc))) { ok = false; break; }
-            reduce_chunk<P>(c, rank, cc, own, cg, root_final, fused, direct);
-            if (signal_parent) {
+            reduce_chunk<P>(c, rank, cc, own, cg, root_final, fused, push);
+            if (publish) {
                 cc_last = cc;
                 if (++pend == PUB) { publish_batch(c, cc_last, G, pend, stamp); pend = 0; }
             }
@@ -690,6 +717,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
 
     trace(c, 2);
     if (!direct) {
+      if (rank != 0) {  // (the root sent to its children inside its final level)
         // receive from the parent at send_level, forward to children at levels send_level-1..0
         float* mine = fused ? w_of(c, rank) : own;
         float* dst[3];
@@ -712,6 +740,7 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
             }
         }
         if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
+      }
     } else {
         cta_barrier(c, rank, 1);
     }
