@@ -50,16 +50,20 @@ def heap_bytes_for(n_floats_total: int, slack: int = 1 << 20) -> int:
     return (hb + (1 << 21) - 1) // (1 << 21) * (1 << 21)
 
 
-def exchange_handles(local: bytes, group=None) -> list:
-    """All-gather every rank's IPC handle over the process group (rank-ordered)."""
+def exchange_handles(local: bytes, group=None, heap_bytes: int = None) -> list:
+    """All-gather every rank's IPC handle over the process group (rank-ordered).
+    With heap_bytes, also checks that every rank allocated the same heap size
+    (symmetric offsets into a smaller peer heap would run past its end)."""
     import torch.distributed as dist
 
     out = [None] * dist.get_world_size(group)
-    dist.all_gather_object(out, bytes(local), group=group)
-    for h in out:
+    dist.all_gather_object(out, (bytes(local), heap_bytes), group=group)
+    for h, hb in out:
         if not isinstance(h, (bytes, bytearray)) or len(h) != _lib.FC_IPC_HANDLE_BYTES:
             raise RuntimeError("malformed IPC handle from a peer")
-    return out
+        if heap_bytes is not None and hb != heap_bytes:
+            raise RuntimeError(f"symmetric heap size differs across ranks: {hb} vs {heap_bytes} bytes")
+    return [h for h, _ in out]
 
 
 def _as_tensor(ptr: int, n: int, device_index: int, typestr: str = "<f4"):
@@ -103,7 +107,7 @@ class World:
         self.heap = heap.value
         hbuf = (ctypes.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
         check(L.firecaffe_heap_export(self.heap, hbuf), "firecaffe_heap_export")
-        handles = exchange_handles(bytes(hbuf), group)
+        handles = exchange_handles(bytes(hbuf), group, self.heap_bytes)
         allh = (ctypes.c_uint8 * (_lib.FC_IPC_HANDLE_BYTES * self.p)).from_buffer_copy(b"".join(handles))
         w = ctypes.c_void_p()
         check(L.firecaffe_world_create(self.rank, self.p, self.device, self.heap, allh, self.heap_bytes,

@@ -23,10 +23,15 @@ def _worker(rank, world, port, q):
     from paper_1511_00175_b200.world import SymmetricLayout, exchange_handles
 
     mine = bytes([rank]) * 64
-    got = exchange_handles(mine)
+    got = exchange_handles(mine, heap_bytes=1 << 30)
     lay = SymmetricLayout(1 << 30, 1 << 20)
     offs = [lay.alloc(n) for n in (4 * 7_600_000, 4 * 7_600_000 + 12, 4 * 5)]
-    q.put((rank, [g[0] for g in got], offs))
+    try:  # a rank with a different heap size is refused on every rank
+        exchange_handles(mine, heap_bytes=(1 << 30) + rank)
+        refused = False
+    except RuntimeError:
+        refused = True
+    q.put((rank, [g[0] for g in got], offs, refused))
     dist.destroy_process_group()
 
 
@@ -43,6 +48,7 @@ def test_handle_exchange_and_symmetric_offsets():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert [r[1] for r in res] == [[0, 1], [0, 1]]  # rank-ordered handles on every rank
+    assert all(r[3] for r in res)  # mismatched heap sizes refused everywhere
     assert res[0][2] == res[1][2]  # identical offsets -> symmetric buffers
     offs = res[0][2]
     assert all(o % 256 == 0 and o >= (1 << 20) for o in offs)
