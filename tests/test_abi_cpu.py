@@ -130,6 +130,26 @@ def test_segment_table_validation_is_host_side():
         assert make(rows, n) == _lib.FC_ERR_INVALID_ARG, rows
 
 
+def test_missing_extension_fails_loudly(monkeypatch, tmp_path):
+    """No fallback: without the built .so every entry point raises (never a CPU path)."""
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(ImportError):
+        fc.firecaffe_version()
+    with pytest.raises(ImportError):
+        fc.firecaffe_scale_lr(0.01, 256, 1024)
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1511_00175_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "oracle.cpp" not in src and "liboracle" not in src, f
+
+
 def test_host_argument_errors_without_gpu():
     L = _lib.load()
     # n < 0 and bad hyper-parameters are rejected before any CUDA call
