@@ -36,8 +36,9 @@ def main():
     rank, p = dist.get_rank(), dist.get_world_size()
     sizes = [int(s) for s in os.environ.get("FC_MP_SIZES", "5,16391,1000003").split(",")]
     nmax = max(sizes)
-    W = fc.World.create(heap_bytes_for(3 * nmax + 4096), timeout_s=float(os.environ.get("FC_MP_TIMEOUT", "20")))
+    W = fc.World.create(heap_bytes_for(3 * nmax + nmax // 2 + 8192), timeout_s=float(os.environ.get("FC_MP_TIMEOUT", "20")))
     grad, w, mom = W.alloc(nmax), W.alloc(nmax), W.alloc(nmax)
+    gb_all = W.alloc(nmax, "bf16")
     scheds = [("forest", "direct"), ("forest", "tree"), ("flat", "direct"), ("single_root", "tree"),
               ("single_root", "direct")]
     if p & (p - 1):
@@ -74,6 +75,32 @@ def main():
         torch.cuda.synchronize()
         if not np.array_equal(bits(grad[:n]), ps_ref.view(np.uint32)):
             fails.append(f"ps n={n}")
+        # bf16 wire, per-blob multipliers, momentum all-gather (FLAT executor)
+        W.config("flat", "direct", 2)
+        gb = gb_all[:n]
+        gb.copy_(g_all[rank].to(torch.bfloat16))
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        fc.firecaffe_tree_allreduce_sgd_bf16(w, gb, mom, world=W, n=n, **HP)
+        torch.cuda.synchronize()
+        wb_ref, _ = oracle.fused_step(g_all.to(torch.bfloat16).float().numpy(), w0.numpy(), v0.numpy(), **HP)
+        if not np.array_equal(bits(w[:n]), wb_ref.view(np.uint32)):
+            fails.append(f"bf16 w n={n}")
+        begins, lm, dm = fc_inputs.caffe_blobs(n)
+        segs = fc.Segments(begins, lm, dm, n)
+        grad[:n].copy_(g_all[rank])
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        fc.firecaffe_tree_allreduce_sgd_segments(w, grad, mom, HP["lr"], HP["mu"], HP["wd"], HP["batch"], segs, W,
+                                                 n=n)
+        fc.firecaffe_allgather_owned(mom, W, n=n)
+        torch.cuda.synchronize()
+        ws_ref, vs_ref = oracle.sgd_segments(w0.numpy(), v0.numpy(), s_ref, **HP, begins=begins, lr_mults=lm,
+                                             decay_mults=dm)
+        if not np.array_equal(bits(w[:n]), ws_ref.view(np.uint32)):
+            fails.append(f"segments w n={n}")
+        if not np.array_equal(bits(mom[:n]), vs_ref.view(np.uint32)):
+            fails.append(f"allgathered mom n={n}")
         # host-buffer entry point (pinned grad in, pinned weights out)
         W.config("flat", "direct", 2)
         g_host = g_all[rank].clone().pin_memory()
