@@ -473,6 +473,52 @@ def test_allgather_owned_momentum_checkpoint(p, sched):
         W.close()
 
 
+@pytest.mark.parametrize("p,k", [(4, 3), (4, 4), (8, 4), (6, 3)])
+def test_virtual_fused_arity_bitexact(p, k):
+    """k-nomial association with the fused update (FLAT executor)."""
+    n = 4096 * 2 + 11
+    W = _world(p, n)
+    try:
+        W.config("flat", "direct", k)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=50 + p + k, dist="mixed")
+        w0, v0 = fc_inputs.weights(n, seed=51), fc_inputs.momentum(n, seed=52)
+        _fill(grads, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+        assert W.poll() == 0
+        w_ref, _ = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **HYPER, k=k)
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+    finally:
+        W.close()
+
+
+def test_degenerate_calls():
+    """n = 0 is a no-op for every call; a 1-rank world's fused call is sgd_step."""
+    W = _world(1, 4100)
+    try:
+        g, w, v = W.alloc(4100)[0], W.alloc(4100)[0], W.alloc(4100)[0]
+        for call in (lambda: fc.firecaffe_tree_allreduce(g, W, n=0),
+                     lambda: fc.firecaffe_ps_allreduce(g, W, n=0),
+                     lambda: fc.firecaffe_allgather_owned(g, W, n=0),
+                     lambda: fc.firecaffe_tree_allreduce_sgd(w, g, v, world=W, n=0, **HYPER),
+                     lambda: fc.firecaffe_sgd_step(w, g, v, n=0, **HYPER)):
+            call()
+        g.copy_(fc_inputs.grad(4100, 0))
+        w.copy_(fc_inputs.weights(4100))
+        v.zero_()
+        w_ref, v_ref = oracle.sgd(w.cpu().numpy(), v.cpu().numpy(), g.cpu().numpy(), **HYPER)
+        fc.firecaffe_tree_allreduce(g, W)  # p = 1: identity
+        fc.firecaffe_tree_allreduce_sgd(w, g, v, world=W, **HYPER)
+        assert W.poll() == 0
+        assert_bitexact(w, w_ref, "w")
+        assert_bitexact(v, v_ref, "v")
+    finally:
+        W.close()
+
+
 def test_sgd_step_vgg19_full_size_every_element():
     """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
     cfg = fc_inputs.CONFIGS["vgg19"]
