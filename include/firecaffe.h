@@ -74,7 +74,9 @@ typedef enum {
 /* How the result goes "back down the tree". Bytes only: value-neutral. */
 typedef enum {
     FC_BCAST_TREE = 0,        /* mirror of the reduce levels (recursive doubling for the forest) */
-    FC_BCAST_DIRECT = 1       /* each owner pushes its slice to every peer in one level */
+    FC_BCAST_DIRECT = 1,      /* each owner pushes its slice to every peer in one level */
+    FC_BCAST_PULL = 2         /* FC_SCHED_FLAT only: owners publish their slice, every rank pulls
+                                 the others (no remote stores, no barrier after the data) */
 } fc_bcast;
 
 typedef struct fc_world fc_world; /* opaque; one per process (or one per virtual world) */

@@ -26,7 +26,8 @@ SCHED = {"forest": FC_SCHED_FOREST, "single_root": FC_SCHED_SINGLE_ROOT, "flat":
 # fc_bcast
 FC_BCAST_TREE = 0
 FC_BCAST_DIRECT = 1
-BCAST = {"tree": FC_BCAST_TREE, "direct": FC_BCAST_DIRECT}
+FC_BCAST_PULL = 2
+BCAST = {"tree": FC_BCAST_TREE, "direct": FC_BCAST_DIRECT, "pull": FC_BCAST_PULL}
 FC_IPC_HANDLE_BYTES = 64
 
 # Every symbol include/firecaffe.h declares: name -> (restype, argtypes)

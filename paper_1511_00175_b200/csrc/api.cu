@@ -272,7 +272,9 @@ fc_status firecaffe_world_destroy(fc_world* w) {
 
 fc_status firecaffe_world_config(fc_world* w, int arity, fc_sched sched, fc_bcast bcast) {
     if (!w) return FC_ERR_INVALID_ARG;
-    if (arity < 2 || (bcast != FC_BCAST_TREE && bcast != FC_BCAST_DIRECT)) return FC_ERR_INVALID_ARG;
+    if (arity < 2 || (bcast != FC_BCAST_TREE && bcast != FC_BCAST_DIRECT && bcast != FC_BCAST_PULL))
+        return FC_ERR_INVALID_ARG;
+    if (bcast == FC_BCAST_PULL && sched != FC_SCHED_FLAT) return FC_ERR_UNSUPPORTED;
     if (sched != FC_SCHED_FOREST && sched != FC_SCHED_SINGLE_ROOT && sched != FC_SCHED_FLAT)
         return FC_ERR_INVALID_ARG;
     if (sched == FC_SCHED_FOREST && (arity != 2 || !is_pow2(w->p))) return FC_ERR_UNSUPPORTED;

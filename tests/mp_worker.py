@@ -39,7 +39,7 @@ def main():
     W = fc.World.create(heap_bytes_for(3 * nmax + nmax // 2 + 8192), timeout_s=float(os.environ.get("FC_MP_TIMEOUT", "20")))
     grad, w, mom = W.alloc(nmax), W.alloc(nmax), W.alloc(nmax)
     gb_all = W.alloc(nmax, "bf16")
-    scheds = [("forest", "direct"), ("forest", "tree"), ("flat", "direct"), ("single_root", "tree"),
+    scheds = [("forest", "direct"), ("forest", "tree"), ("flat", "direct"), ("flat", "pull"), ("single_root", "tree"),
               ("single_root", "direct")]
     if p & (p - 1):
         scheds = [s for s in scheds if s[0] != "forest"]

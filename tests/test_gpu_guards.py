@@ -83,7 +83,7 @@ def test_sgd_step_bf16_and_segments_in_bounds(n):
 
 
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
-@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree"), ("forest", "direct"),
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("flat", "pull"), ("forest", "tree"), ("forest", "direct"),
                                          ("single_root", "tree"), ("single_root", "direct")])
 @pytest.mark.parametrize("n", [5, 4096 * 2 + 3])
 def test_collectives_write_stay_in_bounds(p, sched, bcast, n):

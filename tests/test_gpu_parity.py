@@ -127,7 +127,7 @@ def _fill(dst_list, src_rows):
 
 
 SCHEDS = [("forest", "direct"), ("forest", "tree"), ("single_root", "tree"), ("single_root", "direct"),
-          ("flat", "direct")]
+          ("flat", "direct"), ("flat", "pull")]
 
 
 def _sched_ok(p, sched):
