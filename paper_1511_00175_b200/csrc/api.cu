@@ -656,25 +656,32 @@ fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float
     FcSegs sd;
     st = check_segs(segs, n, &sd);
     if (st != FC_OK) return st;
-    static int64_t chunk = 0;  // floats per pipeline stage (FC_PIPE_CHUNK overrides, for tuning)
-    if (chunk == 0) {
-        const char* e = getenv("FC_PIPE_CHUNK");
-        chunk = e ? atoll(e) : ((int64_t)1 << 21);  // 8 MB stages (scripts/pcie_bench.py)
-        chunk = (chunk + 3) / 4 * 4;
-        if (chunk < 4096) chunk = 4096;
-    }
-    // zero-copy kernel (default) or copy-engine pipeline (FC_HOST_MODE=pipe)
+    // Three host paths (scripts/pcie_bench.py, NiN, B200; PCIe H2D || D2H ceiling 0.66 ms):
+    //   hybrid (default): copy-engine H2D per 4 MB stage, the SGD kernel writes the new
+    //                     weights straight to pinned host memory            0.79 ms
+    //   zc   : one zero-copy kernel (PCIe reads + writes from the SMs)      0.84 ms
+    //   pipe : H2D || SGD || D2H over three streams, 8 MB stages            0.83 ms
+    // FC_HOST_MODE / FC_PIPE_CHUNK override (tuning only; all give the same bits).
     static int mode = -1;
+    static int64_t chunk = 0;  // floats per stage
     if (mode < 0) {
         const char* m = getenv("FC_HOST_MODE");
-        mode = (m && strcmp(m, "pipe") == 0) ? 1 : 0;
+        mode = (m && strcmp(m, "pipe") == 0) ? 1 : (m && strcmp(m, "zc") == 0) ? 0 : 2;
+        const char* e = getenv("FC_PIPE_CHUNK");
+        chunk = e ? atoll(e) : (mode == 1 ? ((int64_t)1 << 21) : ((int64_t)1 << 20));
+        chunk = (chunk + 3) / 4 * 4;
+        if (chunk < 4096) chunk = 4096;
     }
     cudaError_t e;
     const float* gdev = (const float*)device_view(grad_host);
     float* wdev = (float*)device_view(w_host);
-    if (mode == 0 && gdev && wdev && aligned16(gdev) && aligned16(wdev)) {
+    const bool mapped = gdev && wdev && aligned16(gdev) && aligned16(wdev);
+    if (mode == 0 && mapped) {
         e = launch_sgd_step_hostio(w, gdev, grad, mom, wdev, n, lr, mu, wd, inv_batch(batch), sd,
                                    (cudaStream_t)stream);
+    } else if (mode == 2 && mapped) {
+        e = launch_sgd_step_hybrid(w, grad_host, grad, mom, wdev, n, lr, mu, wd, inv_batch(batch), sd,
+                                   chunk, (cudaStream_t)stream);
     } else {
         e = launch_sgd_step_host(w, grad_host, grad, mom, w_host, n, lr, mu, wd, inv_batch(batch), sd,
                                  chunk, (cudaStream_t)stream);

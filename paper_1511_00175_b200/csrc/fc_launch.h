@@ -25,6 +25,10 @@ cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int
                                  cudaStream_t st);
 
 // Host-buffer paths (host_pipeline.cu): zero-copy kernel and copy-engine pipeline
+cudaError_t launch_sgd_step_hybrid(float* w, const float* grad_host, float* grad_dev, float* mom,
+                                   float* w_host_dev, int64_t n, float lr, float mu, float wd,
+                                   float inv_b, const FcSegs& segs, int64_t chunk,
+                                   cudaStream_t user);
 cudaError_t launch_sgd_step_hostio(float* w, const float* grad_host_dev, float* grad_dev, float* mom,
                                    float* w_host_dev, int64_t n, float lr, float mu, float wd,
                                    float inv_b, const FcSegs& segs, cudaStream_t st);

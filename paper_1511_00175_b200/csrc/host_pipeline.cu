@@ -21,7 +21,7 @@ template <int U>
 __global__ void __launch_bounds__(256) sgd_step_hostio_kernel(
     float4* __restrict__ w4, const float4* __restrict__ gh4, float4* __restrict__ gd4,
     float4* __restrict__ v4, float4* __restrict__ wh4, int64_t n4, int64_t n, float lr, float mu,
-    float wd, float inv_b, const FcSegs segs) {
+    float wd, float inv_b, const FcSegs segs, int64_t elem0) {
     const int64_t T = blockDim.x;
     const int64_t stride = (int64_t)gridDim.x * T * U;
     for (int64_t b0 = (int64_t)blockIdx.x * T * U + threadIdx.x; b0 < n4; b0 += stride) {
@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(256) sgd_step_hostio_kernel(
         for (int j = 0; j < U; ++j) {
             const int64_t i = b0 + j * T;
             if (i < n4) {
-                st_na(gd4 + i, g[j]);
-                sgd4_any(segs, 4 * i, g[j], w[j], v[j], lr, mu, wd, inv_b);
+                if (gd4) st_na(gd4 + i, g[j]);
+                sgd4_any(segs, elem0 + 4 * i, g[j], w[j], v[j], lr, mu, wd, inv_b);
                 st_na(w4 + i, w[j]);
                 st_na(v4 + i, v[j]);
                 wh4[i] = w[j];  // PCIe posted write to pinned host memory
@@ -53,9 +53,9 @@ __global__ void __launch_bounds__(256) sgd_step_hostio_kernel(
         const float gg = reinterpret_cast<const float*>(gh4)[e];
         float* wf = reinterpret_cast<float*>(w4);
         float* vf = reinterpret_cast<float*>(v4);
-        reinterpret_cast<float*>(gd4)[e] = gg;
+        if (gd4) reinterpret_cast<float*>(gd4)[e] = gg;
         float ww = wf[e], vv = vf[e];
-        sgd1_any(segs, e, gg, ww, vv, lr, mu, wd, inv_b);
+        sgd1_any(segs, elem0 + e, gg, ww, vv, lr, mu, wd, inv_b);
         wf[e] = ww;
         vf[e] = vv;
         reinterpret_cast<float*>(wh4)[e] = ww;
@@ -75,9 +75,11 @@ cudaError_t launch_sgd_step_hostio(float* w, const float* grad_host, float* grad
     if (grid < 1) grid = 1;
     sgd_step_hostio_kernel<U><<<(unsigned)grid, T, 0, st>>>(
         (float4*)w, (const float4*)grad_host, (float4*)grad_dev, (float4*)mom, (float4*)w_host, n4,
-        n, lr, mu, wd, inv_b, segs);
+        n, lr, mu, wd, inv_b, segs, 0);
     return cudaGetLastError();
 }
+
+
 
 struct PipeCtx {
     bool ready = false;
@@ -148,6 +150,51 @@ cudaError_t launch_sgd_step_host(float* w, const float* grad_host, float* grad_d
     }
     // the user's stream continues after every copy has landed
     if ((e = cudaEventRecord(p->start, p->s[2])) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(user, p->start, 0);
+}
+
+}  // namespace fc
+
+namespace fc {
+
+// Hybrid pipeline: the copy engine brings each stage's gradient in (H2D), the
+// SGD kernel of that stage writes the new weights straight to pinned host
+// memory (SM posted writes), so the two PCIe directions run concurrently
+// without a D2H copy stage.
+cudaError_t launch_sgd_step_hybrid(float* w, const float* grad_host, float* grad_dev, float* mom,
+                                   float* w_host_dev, int64_t n, float lr, float mu, float wd,
+                                   float inv_b, const FcSegs& segs, int64_t chunk,
+                                   cudaStream_t user) {
+    PipeCtx* p = nullptr;
+    cudaError_t e = pipe_ctx(&p);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(p->start, user)) != cudaSuccess) return e;
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaStreamWaitEvent(p->s[i], p->start, 0)) != cudaSuccess) return e;
+    constexpr int U = 4, T = 256;
+    const int occ = occupancy((const void*)sgd_step_hostio_kernel<U>, T);
+    const int64_t cap = (int64_t)dev_info().sms * (occ > 0 ? occ : 1);
+    const int64_t nst = (n + chunk - 1) / chunk;
+    int64_t off = 0;
+    for (int64_t k = 0; k < nst; ++k) {
+        const int64_t len = off + chunk <= n ? chunk : n - off;
+        const int slot = (int)(k % kPipeDepth);
+        if ((e = cudaMemcpyAsync(grad_dev + off, grad_host + off, len * 4, cudaMemcpyHostToDevice,
+                                 p->s[0])) != cudaSuccess)
+            return e;
+        if ((e = cudaEventRecord(p->h2d[slot], p->s[0])) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(p->s[1], p->h2d[slot], 0)) != cudaSuccess) return e;
+        const int64_t n4 = len / 4;
+        int64_t grid = (n4 + (int64_t)T * U - 1) / ((int64_t)T * U);
+        if (grid > cap) grid = cap;
+        if (grid < 1) grid = 1;
+        sgd_step_hostio_kernel<U><<<(unsigned)grid, T, 0, p->s[1]>>>(
+            (float4*)(w + off), (const float4*)(grad_dev + off), nullptr, (float4*)(mom + off),
+            (float4*)(w_host_dev + off), n4, len, lr, mu, wd, inv_b, segs, off);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        off += len;
+    }
+    if ((e = cudaEventRecord(p->start, p->s[1])) != cudaSuccess) return e;
     return cudaStreamWaitEvent(user, p->start, 0);
 }
 
