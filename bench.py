@@ -503,8 +503,9 @@ def main():
             "ms_per_step_warm_l2": round(warm_ms, 5),
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_ms, 4),
-                    "what": ("firecaffe_sgd_step_host: one zero-copy kernel reads the pinned host grad over "
-                             "PCIe, updates w/mom in HBM, writes w to pinned host memory") if N == 1 else
+                    "what": ("firecaffe_sgd_step_host: pinned host grad -> device by the copy engine in 4 MB "
+                             "stages, each stage's SGD kernel writes the new w straight to pinned host memory")
+                            if N == 1 else
                             "firecaffe_tree_allreduce_sgd_host: pinned host grad -> heap, fused tree, w -> host"},
             "gpu_launches": args.steps,
             "gpu_launches_note": "one library kernel per step (L2-flush and barrier kernels are torch/NCCL)",
