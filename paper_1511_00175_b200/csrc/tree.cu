@@ -1,5 +1,6 @@
 // Collective kernels of libfirecaffe: the reduction tree over NVLink peer
-// memory, one persistent cooperative kernel per call.
+// memory: one persistent kernel per call (one wave of CTAs;
+// a cooperative launch for virtual worlds, whose CTAs wait on each other).
 //
 // Every rank's heap is mapped into every process (CUDA IPC), so a kernel reads
 // a peer GPU's gradient slice with ordinary 128-bit loads and writes a peer's
