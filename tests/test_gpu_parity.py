@@ -519,6 +519,56 @@ def test_degenerate_calls():
         W.close()
 
 
+def test_virtual_randomized_trials():
+    """SPEC acceptance 5 shape on the GPU: 40 random (p, executor, arity, n,
+    distribution, op) trials, each bit-exact against the oracle."""
+    rng = np.random.default_rng(20260)
+    ops = ["allreduce", "fused", "ps", "bf16"]
+    for trial in range(40):
+        p = int(rng.integers(2, 9))
+        sched, bcast = SCHEDS[int(rng.integers(0, len(SCHEDS)))]
+        if not _sched_ok(p, sched):
+            sched, bcast = "flat", "direct"
+        k = int(rng.integers(2, p + 1)) if sched == "flat" else 2
+        n = int(rng.integers(1, 60_000))
+        dist = ["paper", "mixed", "cancel", "int"][int(rng.integers(0, 4))]
+        op = ops[int(rng.integers(0, len(ops)))]
+        W = _world(p, n)
+        try:
+            W.config(sched, bcast, k)
+            grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+            gb = W.alloc(n, "bf16") if op == "bf16" else None
+            g = fc_inputs.grads(n, p, seed=trial * 97 + 5, dist=dist)
+            w0, v0 = fc_inputs.weights(n, seed=trial), fc_inputs.momentum(n, seed=trial + 1)
+            _fill(grads, g)
+            _fill(ws, [w0] * p)
+            _fill(moms, [v0] * p)
+            what = f"trial {trial}: p={p} {sched}/{bcast} k={k} n={n} {dist} {op}"
+            if op == "allreduce":
+                fc.firecaffe_tree_allreduce(grads[0], W, n=n)
+                want = oracle.tree_sum(g.numpy(), k)
+                outs = grads
+            elif op == "ps":
+                fc.firecaffe_ps_allreduce(grads[0], W, n=n)
+                want = oracle.ps_sum(g.numpy())
+                outs = grads
+            elif op == "fused":
+                fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, n=n, **HYPER)
+                want, _ = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **HYPER, k=k)
+                outs = ws
+            else:
+                _fill(gb, g.to(torch.bfloat16))
+                fc.firecaffe_tree_allreduce_sgd_bf16(ws[0], gb[0], moms[0], world=W, n=n, **HYPER)
+                want, _ = oracle.fused_step(g.to(torch.bfloat16).float().numpy(), w0.numpy(), v0.numpy(),
+                                            **HYPER, k=k)
+                outs = ws
+            assert W.poll() == 0, what
+            for r in range(p):
+                assert_bitexact(outs[r], want, f"{what} rank {r}")
+        finally:
+            W.close()
+
+
 def test_sgd_step_vgg19_full_size_every_element():
     """Maximum BASELINE size (VGG-19, 143 667 240 params): every element vs the oracle."""
     cfg = fc_inputs.CONFIGS["vgg19"]
