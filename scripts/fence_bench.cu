@@ -41,6 +41,28 @@ __global__ void kern(float4* remote, float4* local, uint32_t* rflag, uint32_t* l
     }
 }
 
+// Warp-level variants of the exit stamp: op 0 = lanes 0..7 each st.release.sys
+// (one store each), op 1 = lane 0 fence.acq_rel.sys then 8 relaxed stores.
+__global__ void kern_warp(float4* remote, uint32_t* rflag, int op, uint64_t* out) {
+    const int t = threadIdx.x, b = blockIdx.x;
+    float4 v = make_float4(1, 2, 3, 4);
+    for (int j = 0; j < 4; ++j) remote[(b * 4 + j) * blockDim.x + t] = v;
+    __syncthreads();
+    uint64_t t0 = gt();
+    if (op == 0) {
+        if (t < 8) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(rflag + b * 8 + t), "r"(1u) : "memory");
+    } else {
+        if (t == 0) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int k = 0; k < 8; ++k)
+                asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(rflag + b * 8 + k), "r"(1u) : "memory");
+        }
+    }
+    __syncwarp();
+    uint64_t t1 = gt();
+    if (t == 0) out[b] = t1 - t0;
+}
+
 int main() {
     int n = 0;
     cudaGetDeviceCount(&n);
@@ -77,6 +99,19 @@ int main() {
             printf("%-16s %-24s median %.0f ns (max-CTA of last rep %llu)\n", moden[mode], opn[op], meds[2],
                    (unsigned long long)h[G - 1]);
         }
+    for (int op = 0; op < 2; ++op) {
+        std::vector<double> meds;
+        for (int rep = 0; rep < 5; ++rep) {
+            kern_warp<<<G, 256>>>(peerbuf, peerflag, op, out);
+            cudaDeviceSynchronize();
+            cudaMemcpy(h.data(), out, G * 8, cudaMemcpyDeviceToHost);
+            std::sort(h.begin(), h.end());
+            meds.push_back((double)h[G / 2]);
+        }
+        std::sort(meds.begin(), meds.end());
+        printf("remote stores    %-40s median %.0f ns\n",
+               op == 0 ? "8 lanes x st.release.sys" : "lane 0: fence.sys + 8 relaxed stores", meds[2]);
+    }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
