@@ -142,6 +142,12 @@ fc_status firecaffe_world_config(fc_world* world, int arity, fc_sched sched, fc_
 fc_status firecaffe_world_get_config(const fc_world* world, int* arity, fc_sched* sched,
                                      fc_bcast* bcast);
 
+/* Cap the CTAs per rank of the collective kernels (0 = automatic: one wave
+ * over all SMs).  A small cap (e.g. 16) lets a collective overlap other work
+ * on the GPU (bucketed overlap with the backward pass) without taking every
+ * SM; every rank must use the same cap.  Value-neutral. */
+fc_status firecaffe_world_set_max_ctas(fc_world* world, int max_ctas);
+
 /* Synchronise the device and return the sticky device status (FC_OK, or
  * FC_ERR_TIMEOUT if any wait of any earlier call timed out). */
 fc_status firecaffe_world_poll(fc_world* world);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "firecaffe_tune_sgd_unroll": (None, [_I]),
     "firecaffe_world_set_trace": (_I, [_P, _P, _I64]),
     "firecaffe_world_last_grid": (_I, [_P]),
+    "firecaffe_world_set_max_ctas": (_I, [_P, _I]),
     "firecaffe_version": (ctypes.c_char_p, []),
     "firecaffe_segments_create": (_I, [_P, _I, _I64, _PP]),
     "firecaffe_segments_destroy": (_I, [_P]),

@@ -43,6 +43,7 @@ struct fc_world {
     uint64_t* trace;
     int64_t trace_cap;
     int last_grid;
+    int max_ctas;  // 0 = automatic
 };
 
 namespace fc {
@@ -456,8 +457,9 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.red_words = w->layout.red_words;
     c.max_chunks = w->layout.max_chunks;
     const int sched = (op == FC_OP_PS || bf16) ? FC_SCHED_FLAT : w->sched;
-    const int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op, n);
+    int grid = collective_grid(sched, w->arity, w->p, w->virt != 0, op, n);
     if (grid < 1) return FC_ERR_UNSUPPORTED;
+    if (w->max_ctas > 0 && grid > w->max_ctas) grid = w->max_ctas;
     w->last_grid = grid;
     const int64_t need = (int64_t)grid * (w->virt ? w->p : 1) * FC_TRACE_SLOTS;
     c.trace = (w->trace && w->trace_cap >= need) ? w->trace : nullptr;
@@ -753,5 +755,11 @@ fc_status firecaffe_world_set_trace(fc_world* w, uint64_t* buf, int64_t capacity
 }
 
 int firecaffe_world_last_grid(const fc_world* w) { return w ? w->last_grid : 0; }
+
+fc_status firecaffe_world_set_max_ctas(fc_world* w, int max_ctas) {
+    if (!w || max_ctas < 0 || max_ctas > FC_MAX_CTAS) return FC_ERR_INVALID_ARG;
+    w->max_ctas = max_ctas;
+    return FC_OK;
+}
 
 }  // extern "C"

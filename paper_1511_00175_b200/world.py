@@ -165,6 +165,10 @@ class World:
         b = _lib.BCAST[bcast] if isinstance(bcast, str) else int(bcast)
         check(load().firecaffe_world_config(self.handle, int(arity), s, b), "firecaffe_world_config")
 
+    def set_max_ctas(self, max_ctas: int):
+        """Cap the collective's CTAs per rank (0 = all SMs); e.g. 16 to overlap with compute."""
+        check(load().firecaffe_world_set_max_ctas(self.handle, int(max_ctas)), "firecaffe_world_set_max_ctas")
+
     def get_config(self):
         a, s, b = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         check(load().firecaffe_world_get_config(self.handle, ctypes.byref(a), ctypes.byref(s), ctypes.byref(b)),
