@@ -519,6 +519,32 @@ def test_degenerate_calls():
         W.close()
 
 
+@pytest.mark.parametrize("max_ctas", [1, 3, 16])
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree"), ("single_root", "tree")])
+def test_capped_grid_is_value_neutral(max_ctas, sched, bcast):
+    """firecaffe_world_set_max_ctas (overlap with compute) changes only the launch."""
+    p, n = 4, 4096 * 9 + 3
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        W.set_max_ctas(max_ctas)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=31 + max_ctas)
+        w0, v0 = fc_inputs.weights(n, seed=32), fc_inputs.momentum(n, seed=33)
+        _fill(grads, g)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+        assert W.poll() == 0
+        w_ref, _ = oracle.fused_step(g.numpy(), w0.numpy(), v0.numpy(), **HYPER)
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+        with pytest.raises(fc.FcError):
+            W.set_max_ctas(-1)
+    finally:
+        W.close()
+
+
 def test_virtual_randomized_trials():
     """SPEC acceptance 5 shape on the GPU: 40 random (p, executor, arity, n,
     distribution, op) trials, each bit-exact against the oracle."""
