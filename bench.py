@@ -425,7 +425,10 @@ def main():
                 "kernel": f"fc::{cfgw['sched']}_kernel ({cfgw['bcast']} broadcast)",
                 "alg_bytes_per_launch": alg_bytes,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction (nominal 900)",
-                "frac_of_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)}
+                "frac_of_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4),
+                # this traffic's own measured ceiling (both directions loaded, SM loads+stores;
+                # scripts/nvlink_bench.cu, profiles/r01_nvlink_bench_sm.txt)
+                "frac_of_measured_bidirectional_690": round(achieved / 690.0, 4)}
 
     # ---- baselines on the same buffers (context: PS, paper's single-root tree, NCCL, torch)
     baselines = {}
