@@ -111,6 +111,27 @@ def main():
         torch.cuda.synchronize()
         if not np.array_equal(w_host.numpy().view(np.uint32), w_ref.view(np.uint32)):
             fails.append(f"host entry w n={n}")
+    # back-to-back fused steps across real GPUs, no host synchronisation between
+    # them (each rank refreshes its own gradient with a stream-ordered copy)
+    n = sizes[-1]
+    for sched, bcast in (("flat", "direct"), ("forest" if not (p & (p - 1)) else "flat", "tree" if not (p & (p - 1))
+                                                                                   else "pull")):
+        W.config(sched, bcast, 2)
+        gsteps = [fc_inputs.grads(n, p, seed=9000 + s) for s in range(6)]
+        mine = [g[rank].to(dev) for g in gsteps]
+        w0, v0 = fc_inputs.weights(n, seed=61), fc_inputs.momentum(n, seed=62)
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        torch.cuda.synchronize()
+        for s in range(6):
+            grad[:n].copy_(mine[s], non_blocking=True)
+            fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, n=n, **HP)
+        torch.cuda.synchronize()
+        wr, vr = w0.numpy(), v0.numpy()
+        for s in range(6):
+            wr, vr = oracle.fused_step(gsteps[s].numpy(), wr, vr, **HP)
+        if not np.array_equal(bits(w[:n]), wr.view(np.uint32)):
+            fails.append(f"back-to-back {sched}/{bcast}")
     st = W.poll()
     if st != 0:
         fails.append(f"device status {st}")

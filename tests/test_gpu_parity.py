@@ -545,6 +545,43 @@ def test_capped_grid_is_value_neutral(max_ctas, sched, bcast):
         W.close()
 
 
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree"), ("forest", "direct"),
+                                         ("single_root", "tree"), ("flat", "pull")])
+def test_back_to_back_steps_without_host_sync(sched, bcast):
+    """12 fused steps (and interleaved allreduce / PS / allgather calls) queued
+    back to back on one stream, gradients refreshed by stream-ordered copies,
+    no host synchronisation: flags and epochs must carry across calls."""
+    p, n, steps = 4, 4096 * 5 + 9, 12
+    W = _world(p, n, bufs=5)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms, scratch = W.alloc(n), W.alloc(n), W.alloc(n), W.alloc(n)
+        gs = [fc_inputs.grads(n, p, seed=700 + s).cuda() for s in range(steps)]
+        w0, v0 = fc_inputs.weights(n, seed=7), fc_inputs.momentum(n, seed=8)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        for s in range(steps):
+            for r in range(p):
+                grads[r].copy_(gs[s][r], non_blocking=True)
+                scratch[r].copy_(gs[s][(r + s) % p], non_blocking=True)
+            fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+            if s % 3 == 0:
+                fc.firecaffe_tree_allreduce(scratch[0], W)
+            elif s % 3 == 1:
+                fc.firecaffe_ps_allreduce(scratch[0], W)
+        fc.firecaffe_allgather_owned(moms[0], W)
+        torch.cuda.synchronize()
+        assert W.poll() == 0
+        w, v = w0.numpy(), v0.numpy()
+        for s in range(steps):
+            w, v = oracle.fused_step(gs[s].cpu().numpy(), w, v, **HYPER)
+        for r in range(p):
+            assert_bitexact(ws[r], w, f"w rank {r}")
+            assert_bitexact(moms[r], v, f"mom rank {r}")
+    finally:
+        W.close()
+
+
 def test_virtual_randomized_trials():
     """SPEC acceptance 5 shape on the GPU: 40 random (p, executor, arity, n,
     distribution, op) trials, each bit-exact against the oracle."""
