@@ -8,10 +8,13 @@ contracted).  -lineinfo so ncu's source page maps to csrc/.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -24,7 +27,6 @@ NVCC_FLAGS = [
     "-lineinfo",
     "--fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-Xcompiler", "-fPIC,-O2",
-    "-shared",
     "-diag-suppress", "20281",
 ]
 
@@ -45,17 +47,32 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC, *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *sources()]
+def _run(cmd):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    if verbose:
-        sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
+        raise RuntimeError("nvcc failed: " + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every csrc/*.cu to an object in parallel (the kernel tables are
+    split over several translation units), then link the shared library."""
+    if not force and up_to_date():
+        return LIB
+    tmpdir = tempfile.mkdtemp(prefix="fc_build_")
+    try:
+        srcs = sources()
+        objs = [os.path.join(tmpdir, os.path.basename(s) + ".o") for s in srcs]
+        extra = ["-Xptxas", "-v"] if verbose else []
+        with concurrent.futures.ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+            logs = list(ex.map(_run, [[NVCC, *NVCC_FLAGS, *extra, "-c", s, "-o", o] for s, o in zip(srcs, objs)]))
+        tmp = LIB + ".tmp%d" % os.getpid()
+        _run([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs])
+        if verbose:
+            sys.stderr.write("".join(logs))
+        os.replace(tmp, LIB)
+    finally:
+        shutil.rmtree(tmpdir, ignore_errors=True)
     return LIB
 
 

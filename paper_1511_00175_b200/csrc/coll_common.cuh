@@ -1,0 +1,296 @@
+// Device-side building blocks shared by the collective executors
+// (coll_flat.cu, coll_tree.cu): heap addressing, the device epoch counter,
+// the cross-GPU CTA barrier, batched flag publication and the chunk
+// operations of the tree schedules.  Included by exactly those .cu files.
+//
+// Every rank's heap is mapped into every process (CUDA IPC), so a kernel reads
+// a peer GPU's gradient slice with ordinary 128-bit loads and writes a peer's
+// weights with ordinary 128-bit stores; both cross NVLink / NVSwitch.  Order
+// between GPUs comes from epoch-stamped flags in the heaps' reserved prefix
+// (st.release.sys / ld.acquire.sys).  Producers PUSH flags to the consumer's
+// heap so that every spin is on local memory.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fc_device.cuh"
+#include "fc_launch.h"
+
+namespace fc {
+
+constexpr int TREE_T = kTreeThreads;              // threads per CTA (tree schedules)
+constexpr int FLAT_T = kFlatThreads;              // threads per CTA (FLAT / PS), one CTA per SM
+// float4 per thread per operand in flight in FLAT: enough remote bytes in flight
+// (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
+// (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*)
+#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : 2)
+constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
+constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
+static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
+
+// ------------------------------------------------------------ addressing ---
+__device__ __forceinline__ int my_rank(const FcColl& c) {
+    return c.rank >= 0 ? c.rank : (int)blockIdx.y;
+}
+__device__ __forceinline__ uint32_t* flag_base(const FcColl& c, int q) {
+    return reinterpret_cast<uint32_t*>(c.peers.heap[q]);
+}
+__device__ __forceinline__ uint64_t* bar_flag(const FcColl& c, int owner, int slot, int cta,
+                                              int src) {
+    return reinterpret_cast<uint64_t*>(flag_base(c, owner)) +
+           ((int64_t)(slot * FC_MAX_CTAS + cta) * FC_MAX_RANKS + src);
+}
+__device__ __forceinline__ uint32_t* red_flag(const FcColl& c, int owner, int l, int64_t cc) {
+    return flag_base(c, owner) + c.bar_words + (int64_t)l * c.max_chunks + cc;
+}
+__device__ __forceinline__ uint32_t* av_flag(const FcColl& c, int owner, int64_t cc) {
+    return flag_base(c, owner) + c.red_words + cc;
+}
+__device__ __forceinline__ float* grad_of(const FcColl& c, int q) {
+    return reinterpret_cast<float*>(c.peers.heap[q] + c.off_grad);
+}
+__device__ __forceinline__ float* w_of(const FcColl& c, int q) {
+    return reinterpret_cast<float*>(c.peers.heap[q] + c.off_w);
+}
+__device__ __forceinline__ float* mom_of(const FcColl& c, int q) {
+    return c.off_mom >= 0 ? reinterpret_cast<float*>(c.peers.heap[q] + c.off_mom) : c.mom_local;
+}
+
+__device__ __forceinline__ void trace(const FcColl& c, int slot) {
+    if (c.trace && threadIdx.x == 0)
+        c.trace[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * FC_TRACE_SLOTS + slot] = globaltimer();
+}
+
+// ------------------------------------------------------------ epochs -------
+// The call counter lives in device memory (c.ctl[0] = epoch of the last
+// completed call, c.ctl[1] = CTAs finished in the current call), so a call's
+// kernel arguments never change from call to call and the collectives can be
+// captured in a CUDA graph and replayed.  Every CTA reads the epoch at entry;
+// the last CTA to finish publishes the next one (stream order makes it visible
+// to the next launch).  All ranks make the same calls, so the counters agree.
+__shared__ uint32_t s_epoch;
+
+__device__ __forceinline__ void epoch_begin(const FcColl& c) {
+    if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)c.ctl + 1u;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void epoch_end(const FcColl& c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * gridDim.y;
+        const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
+        if (done == total) {
+            c.ctl[1] = 0u;
+            __threadfence();
+            atomicExch(c.ctl, s_epoch);
+        }
+    }
+}
+
+// ------------------------------------------------------------ sync ---------
+// All-to-all barrier among the CTAs with this blockIdx.x on every rank
+// (slot 0 = entry, 1 = exit).  Thread q < p pushes "rank arrived" into rank q's
+// heap, then spins on rank q's stamp in the local heap.
+//  entry (slot 0): the stamp orders nothing the CTA wrote (the rank's inputs
+//    were produced by earlier kernels, complete and coherent in its L2), so it
+//    is a relaxed store: no fence on the critical path.
+//  exit (slot 1): st.release.sys orders the CTA's earlier writes — peer stores
+//    included; the __syncthreads orders the other threads' writes before it
+//    (PTX causality through bar.sync) — ahead of the stamp.
+// A stamp is one 64-bit word: epoch | signature << 32.  The signature hashes the
+// call's op, n, executor and hyper-parameters; a peer whose signature differs
+// made a different call (MPI/NCCL rule broken) -> sticky FC_ERR_MISMATCH on
+// every rank and no data is touched.
+static __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
+    __syncthreads();
+    const int t = threadIdx.x;
+    bool good = true;
+    if (t < c.p && t != rank) {
+        const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
+        uint64_t* dst = bar_flag(c, t, slot, blockIdx.x, rank);
+        if (slot == 0) st_relaxed_sys64(dst, stamp);
+        else st_release_sys64(dst, stamp);
+        const uint64_t* f = bar_flag(c, rank, slot, blockIdx.x, t);
+        uint64_t v = ld_acquire_sys64(f);
+        if (!reached((uint32_t)v, s_epoch)) {
+            const uint64_t t0 = globaltimer();
+            uint32_t spins = 0;
+            while (true) {
+                v = ld_relaxed_sys64(f);
+                if (reached((uint32_t)v, s_epoch)) {
+                    v = ld_acquire_sys64(f);
+                    break;
+                }
+                if ((++spins & 63u) == 0) {
+                    if (*(volatile int*)c.status != FC_OK) { good = false; break; }
+                    if (globaltimer() - t0 > c.timeout_ns) {
+                        atomicCAS(c.status, FC_OK, FC_ERR_TIMEOUT);
+                        good = false;
+                        break;
+                    }
+                }
+            }
+        }
+        if (good && (uint32_t)v == s_epoch && (uint32_t)(v >> 32) != c.sig) {
+            atomicCAS(c.status, FC_OK, FC_ERR_MISMATCH);
+            good = false;
+        }
+    }
+    return __syncthreads_and(good) != 0;
+}
+
+// One thread waits for a flag; the CTA learns the outcome.
+__device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
+    bool good = true;
+    if (threadIdx.x == 0) good = wait_flag(f, s_epoch, c.timeout_ns, c.status);
+    return __syncthreads_and(good) != 0;
+}
+
+// Publish the CTA's last `count` chunks (cc_last, cc_last - G, ...) after ONE
+// sys-scope release fence: thread 0 fences (ordering every thread's chunk
+// writes, sequenced before it by the bar.sync) and then writes the consumers'
+// epoch stamps with relaxed stores (`stamp(cc)` does the stores for one
+// chunk).  A sys fence costs 4-8 us on B200 (scripts/fence_bench.cu), so the
+// tree schedules pay one per PUB chunks instead of one per chunk.
+constexpr int PUB = 8;
+template <typename Stamp>
+__device__ __forceinline__ void publish_batch(const FcColl& c, int64_t cc_last, int G, int count,
+                                              Stamp stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_sys();
+        for (int k = 0; k < count; ++k) stamp(cc_last - (int64_t)k * G);
+    }
+}
+
+__device__ __forceinline__ int64_t first_chunk(int64_t lo, int G, int b) {
+    const int64_t r = lo % G;
+    return lo + ((b - r) % G + G) % G;
+}
+
+// ------------------------------------------------------------ chunk ops ----
+// Level step on chunk cc: s = own partial + peer partial (R1: the
+// lower rank group's partial plus the upper group's; fp32 addition commutes
+// bitwise, so operand order is immaterial).  Not last: s -> own grad (in
+// place).  Last (subtree root): fused -> SGD on w, mom; unfused -> s -> grad.
+// `push`: bitmask of ranks that also receive the result right away (last level
+// only): every other rank for a direct broadcast, the first broadcast hop for
+// a tree broadcast, so the root's link sends while it still receives.
+template <int P>
+__device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t cc, float* own,
+                                             const float* peer, bool last, bool fused,
+                                             uint32_t push) {
+    const int64_t e0 = cc * FC_CHUNK_FLOATS;
+    const int64_t e1 = min(e0 + (int64_t)FC_CHUNK_FLOATS, c.n);
+    const int nf4 = (int)((e1 - e0) >> 2);
+    const int rem = (int)((e1 - e0) & 3);
+    const int t = threadIdx.x;
+    float4* own4 = reinterpret_cast<float4*>(own + e0);
+    const float4* peer4 = reinterpret_cast<const float4*>(peer + e0);
+    float4 a[PER_T], b[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            a[j] = ld_cg(own4 + k);
+            b[j] = ld_cg(peer4 + k);
+        }
+    }
+    if (!last || !fused) {
+#pragma unroll
+        for (int j = 0; j < PER_T; ++j) {
+            const int k = j * TREE_T + t;
+            if (k < nf4) {
+                const float4 s = add4(a[j], b[j]);
+                st_na(own4 + k, s);
+                if (last && push) {
+#pragma unroll
+                    for (int q = 0; q < P; ++q)
+                        if ((push >> q) & 1u) st_na(reinterpret_cast<float4*>(grad_of(c, q) + e0) + k, s);
+                }
+            }
+        }
+        if (t < rem) {
+            const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+            const float s = __fadd_rn(ld_cg1(own + e), ld_cg1(peer + e));
+            st1(own + e, s);
+            if (last && push)
+                for (int q = 0; q < P; ++q)
+                    if ((push >> q) & 1u) st1(grad_of(c, q) + e, s);
+        }
+        return;
+    }
+    // last level, fused SGD: the reduced gradient lives only in registers
+    float4* w4 = reinterpret_cast<float4*>(w_of(c, rank) + e0);
+    float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank) + e0);
+    float4 w[PER_T], v[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            w[j] = ld_rw(w4 + k);
+            v[j] = ld_rw(v4 + k);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) {
+            const float4 s = add4(a[j], b[j]);
+            sgd4_any(c.segs, e0 + 4 * (int64_t)k, s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+            st_na(w4 + k, w[j]);
+            st_na(v4 + k, v[j]);
+            if (push) {
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if ((push >> q) & 1u) st_na(reinterpret_cast<float4*>(w_of(c, q) + e0) + k, w[j]);
+            }
+        }
+    }
+    if (t < rem) {
+        const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+        const float s = __fadd_rn(ld_cg1(own + e), ld_cg1(peer + e));
+        float* wp = w_of(c, rank) + e;
+        float* vp = mom_of(c, rank) + e;
+        float ww = *wp, vv = *vp;
+        sgd1_any(c.segs, e, s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+        st1(wp, ww);
+        st1(vp, vv);
+        if (push)
+            for (int q = 0; q < P; ++q)
+                if ((push >> q) & 1u) st1(w_of(c, q) + e, ww);
+    }
+}
+
+// Copy chunk cc of `src` (local) to up to 3 destinations (peers).
+__device__ __forceinline__ void copy_chunk(const FcColl& c, int64_t cc, const float* src,
+                                           float* const* dst, int ndst) {
+    const int64_t e0 = cc * FC_CHUNK_FLOATS;
+    const int64_t e1 = min(e0 + (int64_t)FC_CHUNK_FLOATS, c.n);
+    const int nf4 = (int)((e1 - e0) >> 2);
+    const int rem = (int)((e1 - e0) & 3);
+    const int t = threadIdx.x;
+    const float4* s4 = reinterpret_cast<const float4*>(src + e0);
+    float4 x[PER_T];
+#pragma unroll
+    for (int j = 0; j < PER_T; ++j) {
+        const int k = j * TREE_T + t;
+        if (k < nf4) x[j] = ld_cg(s4 + k);
+    }
+    for (int d = 0; d < ndst; ++d) {
+        float4* d4 = reinterpret_cast<float4*>(dst[d] + e0);
+#pragma unroll
+        for (int j = 0; j < PER_T; ++j) {
+            const int k = j * TREE_T + t;
+            if (k < nf4) st_na(d4 + k, x[j]);
+        }
+    }
+    if (t < rem) {
+        const int64_t e = e0 + 4 * (int64_t)nf4 + t;
+        const float v = ld_cg1(src + e);
+        for (int d = 0; d < ndst; ++d) st1(dst[d] + e, v);
+    }
+}
+
+}  // namespace fc

@@ -1,0 +1,209 @@
+// The fp32 FLAT executor kernel template: one
+// NVSwitch round per call.  Instantiated once per unroll factor U in
+// coll_flat_u{1,2,4}.cu (FC_FLAT_TABLE below) so the ~80 <P, K, U> variants
+// compile in parallel; see coll_common.cuh for the synchronisation.
+#pragma once
+#include "coll_common.cuh"
+
+namespace fc {
+
+// ------------------------------------------------------------ FLAT / PS ----
+// One communication level: the owner of slice [e0, e1) loads all P ranks'
+// values, evaluates the K-nomial tree in registers (K = P: the parameter
+// server's sequential order), then either applies SGD and pushes w' to every
+// rank (fused) or pushes the sum to every rank's grad.
+// Pull broadcast (FC_BCAST_PULL): copy every peer's published slice elements
+// produced by the peer CTA with this CTA's index (same grid-stride mapping).
+template <int P, int U>
+__device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
+    const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
+    const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    int64_t b0[P], len4[P];
+    int64_t maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        int64_t c0, c1;
+        owned_chunks(q, P, nch, false, &c0, &c1);
+        const int64_t e0 = c0 * FC_CHUNK_FLOATS, e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+        b0[q] = e0 / 4;
+        len4[q] = e1 > e0 ? e1 / 4 - e0 / 4 : 0;
+        if (q != rank && len4[q] > maxlen) maxlen = len4[q];
+    }
+    const float4* src[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const float4*>(fused ? w_of(c, q) : grad_of(c, q));
+    float4* dst = reinterpret_cast<float4*>(fused ? w_of(c, rank) : grad_of(c, rank));
+    const int64_t T = FLAT_T;
+    const int64_t stride = (int64_t)gridDim.x * T * U;
+    for (int64_t rel = (int64_t)blockIdx.x * T * U + threadIdx.x; rel < maxlen; rel += stride) {
+        float4 x[U][P];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+                if (q != rank && rel + j * T < len4[q]) x[j][q] = ld_cg(src[q] + b0[q] + rel + j * T);
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+#pragma unroll
+            for (int q = 0; q < P; ++q)
+                if (q != rank && rel + j * T < len4[q]) st_na(dst + b0[q] + rel + j * T, x[j][q]);
+    }
+    if (blockIdx.x == 0) {  // trailing n % 4 elements of the last slice
+        for (int q = 0; q < P; ++q) {
+            if (q == rank) continue;
+            int64_t c0, c1;
+            owned_chunks(q, P, nch, false, &c0, &c1);
+            const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+            if (e1 <= c0 * FC_CHUNK_FLOATS) continue;
+            const int64_t e = 4 * (b0[q] + len4[q]) + threadIdx.x;
+            if (e < e1) {
+                const float* s1 = fused ? w_of(c, q) : grad_of(c, q);
+                float* d1 = fused ? w_of(c, rank) : grad_of(c, rank);
+                st1(d1 + e, ld_cg1(s1 + e));
+            }
+        }
+    }
+}
+
+template <int P, int K, int U>
+__global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
+    const int rank = my_rank(c);
+    const bool pull = c.bcast == FC_BCAST_PULL && c.op != FC_OP_PS;
+    epoch_begin(c);
+    trace(c, 0);
+    const bool ok = cta_barrier(c, rank, 0);
+    trace(c, 1);
+    if (ok) {
+        const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+        int64_t c0, c1;
+        owned_chunks(rank, P, nch, c.op == FC_OP_PS, &c0, &c1);
+        const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+        const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+        const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
+        if (e1 > e0) {
+            // push broadcast: results go to every rank's buffer now; pull broadcast:
+            // only to the own buffer, the peers fetch them after the publish barrier
+            const int64_t i0 = e0 / 4, i1 = e1 / 4;
+            const int64_t T = FLAT_T;
+            // grid-stride: all CTAs sweep the slice in lockstep, so at any moment the
+            // GPU's remote reads fall in one few-MB window of each peer's heap (a
+            // contiguous range per CTA measured ~10% slower: 444 scattered streams)
+            const int64_t ce = i1;
+            const int64_t stride = (int64_t)gridDim.x * T * U;
+            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < ce;
+                 base += stride) {
+                float4 x[U][P];
+#pragma unroll
+                for (int j = 0; j < U; ++j) {
+                    const int64_t i = base + j * T;
+                    if (i < ce) {
+#pragma unroll
+                        for (int q = 0; q < P; ++q)
+                            x[j][q] = ld_cg(reinterpret_cast<const float4*>(grad_of(c, q)) + i);
+                    }
+                }
+                if (fused) {
+                    float4 w[U], v[U];
+                    float4* w4 = reinterpret_cast<float4*>(w_of(c, rank));
+                    float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < ce) {
+                            w[j] = ld_rw(w4 + i);
+                            v[j] = ld_rw(v4 + i);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < ce) {
+                            const float4 S = tree_sum_regs<P, K>(x[j]);
+                            sgd4_any(c.segs, 4 * i, S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                            st_na(v4 + i, v[j]);
+#pragma unroll
+                            for (int q = 0; q < P; ++q)
+                                if (!pull || q == rank) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int64_t i = base + j * T;
+                        if (i < ce) {
+                            const float4 S = tree_sum_regs<P, K>(x[j]);
+#pragma unroll
+                            for (int q = 0; q < P; ++q)
+                                if (!pull || q == rank) st_na(reinterpret_cast<float4*>(grad_of(c, q)) + i, S);
+                        }
+                    }
+                }
+            }
+            // trailing n % 4 elements of the last slice
+            const int rem = (int)(e1 - 4 * i1);
+            if (blockIdx.x == 0 && (int)threadIdx.x < rem) {
+                const int64_t e = 4 * i1 + threadIdx.x;
+                float xs[P];
+#pragma unroll
+                for (int q = 0; q < P; ++q) xs[q] = ld_cg1(grad_of(c, q) + e);
+                const float S = tree_sum_regs1<P, K>(xs);
+                if (fused) {
+                    float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
+                    sgd1_any(c.segs, e, S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                    st1(mom_of(c, rank) + e, vv);
+                    for (int q = 0; q < P; ++q)
+                        if (!pull || q == rank) st1(w_of(c, q) + e, ww);
+                } else {
+                    for (int q = 0; q < P; ++q)
+                        if (!pull || q == rank) st1(grad_of(c, q) + e, S);
+                }
+            }
+        }
+    }
+    trace(c, 2);
+    // push: the exit barrier proves every peer's stores into this rank landed.
+    // pull: the same barrier, now BEFORE the broadcast, publishes this CTA's
+    // finished results (release after local stores only); then this CTA copies
+    // the matching elements of every peer's slice (the ones that peer's CTA
+    // with the same index produced) and the kernel ends with no remote writes.
+    const bool ok2 = cta_barrier(c, rank, 1);
+    if (pull && ok && ok2) pull_results<P, U>(c, rank);
+    trace(c, 3);
+    epoch_end(c);
+}
+
+// Kernel table of one unroll factor: flat_kernel<p, arity, U> (arity >= p is
+// the same association as arity = p: one level, sequential).
+#define FC_FLAT_TABLE(U)                                                                     \
+    template <int P>                                                                         \
+    static const void* flat_for_##U(int K) {                                                 \
+        if (K >= P) K = P;                                                                   \
+        switch (K) {                                                                         \
+            case 2: return (const void*)flat_kernel<P, 2, U>;                                \
+            case 3: if constexpr (P >= 3) return (const void*)flat_kernel<P, 3, U>; break;   \
+            case 4: if constexpr (P >= 4) return (const void*)flat_kernel<P, 4, U>; break;   \
+            case 5: if constexpr (P >= 5) return (const void*)flat_kernel<P, 5, U>; break;   \
+            case 6: if constexpr (P >= 6) return (const void*)flat_kernel<P, 6, U>; break;   \
+            case 7: if constexpr (P >= 7) return (const void*)flat_kernel<P, 7, U>; break;   \
+            case 8: if constexpr (P >= 8) return (const void*)flat_kernel<P, 8, U>; break;   \
+        }                                                                                    \
+        return nullptr;                                                                      \
+    }                                                                                        \
+    const void* flat_kernel_u##U(int p, int arity) {                                         \
+        switch (p) {                                                                         \
+            case 2: return flat_for_##U<2>(arity);                                           \
+            case 3: return flat_for_##U<3>(arity);                                           \
+            case 4: return flat_for_##U<4>(arity);                                           \
+            case 5: return flat_for_##U<5>(arity);                                           \
+            case 6: return flat_for_##U<6>(arity);                                           \
+            case 7: return flat_for_##U<7>(arity);                                           \
+            case 8: return flat_for_##U<8>(arity);                                           \
+        }                                                                                    \
+        return nullptr;                                                                      \
+    }
+
+const void* flat_kernel_u1(int p, int arity);
+const void* flat_kernel_u2(int p, int arity);
+const void* flat_kernel_u4(int p, int arity);
+
+}  // namespace fc

@@ -44,6 +44,15 @@ cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, 
 // Max CTAs per rank that can be co-resident for this schedule (virt: divided by p).
 int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n);
 
+// Kernel tables (nullptr if no instantiation exists for that p / arity).
+constexpr int kTreeThreads = 256;  // threads per CTA, FOREST / SINGLE_ROOT
+constexpr int kFlatThreads = 512;  // threads per CTA, FLAT / PS / bf16 / all-gather
+const void* flat_kernel_for(int p, int arity);       // coll_flat.cu (also PS: arity = p)
+const void* flat_bf16_kernel_for(int p, int arity);  // coll_flat.cu
+const void* allgather_kernel_for(int p);             // coll_flat.cu
+const void* forest_kernel_for(int p);                // coll_tree.cu
+const void* single_root_kernel_for(int p);           // coll_tree.cu
+
 // Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
 __host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }
 __host__ __device__ inline void owned_chunks(int rank, int p, int64_t n_chunks, bool single_root,
