@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """PCIe ceiling for the e2e number: pinned H2D, D2H, and both concurrently on
 two streams (30.4 MB each = NiN), plus firecaffe_sgd_step_host at several
-pipeline chunk sizes (run once per FC_PIPE_CHUNK value)."""
+pipeline chunk sizes (run once per FC_HOST_MODE / FC_PIPE_CHUNK value)."""
 import json
 import os
 import sys
@@ -53,4 +53,5 @@ import paper_1511_00175_b200 as fc  # noqa: E402
 w, m = torch.randn(n, device="cuda"), torch.zeros(n, device="cuda")
 res["sgd_step_host_ms"] = round(t(lambda: fc.firecaffe_sgd_step_host(w, d, m, h_in, h_out, 0.04, 0.9, 5e-4, 1024)), 4)
 res["chunk"] = os.environ.get("FC_PIPE_CHUNK", "default")
+res["mode"] = os.environ.get("FC_HOST_MODE", "hybrid")
 print(json.dumps(res))

@@ -7,6 +7,9 @@ from fc_inputs (shared generator, no method arithmetic).  Sizes span several
 world (p ranks on one GPU, one cooperative kernel) — the same kernels the real
 world launches with one rank per GPU (tests/test_multi_gpu.py).
 """
+import os
+import sys
+
 import numpy as np
 import pytest
 import torch
@@ -19,6 +22,7 @@ pytestmark = pytest.mark.gpu
 fc = pytest.importorskip("paper_1511_00175_b200")
 
 HYPER = dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024)  # NiN
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SIZES = [1, 3, 4, 5, 4095, 4096, 4097, 3 * 4096 + 7, 100_003, (1 << 20) + 5]
 
 
@@ -360,6 +364,42 @@ def test_sgd_step_host_pipeline_bitexact(n, with_segs):
     assert_bitexact(g_dev, g.numpy(), "grad copied")
     with pytest.raises(ValueError):  # pageable host memory is refused
         fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g, w_host, **HYPER)
+
+
+_HOST_MODE_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import fc_inputs, oracle, paper_1511_00175_b200 as fc
+HYPER = dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024)
+bad = 0
+for n in (5, 4096 * 7 + 3, 50_003, 3 * (1 << 20) + 7):
+    g = fc_inputs.grad(n, 0, seed=n + 31)
+    w, v = fc_inputs.weights(n, seed=32), fc_inputs.momentum(n, seed=33)
+    b, lm, dm = fc_inputs.caffe_blobs(n)
+    segs = fc.Segments(b, lm, dm, n)
+    w_ref, v_ref = oracle.sgd_segments(w.numpy(), v.numpy(), g.numpy(), **HYPER, begins=b, lr_mults=lm, decay_mults=dm)
+    g_host, w_host = g.pin_memory(), torch.full((n,), float("nan")).pin_memory()
+    w_dev, v_dev, g_dev = w.cuda(), v.cuda(), torch.empty(n, device="cuda")
+    fc.firecaffe_sgd_step_host(w_dev, g_dev, v_dev, g_host, w_host, **HYPER, segs=segs)
+    torch.cuda.synchronize()
+    for name, got, ref in (("w_host", w_host, w_ref), ("w", w_dev.cpu(), w_ref), ("v", v_dev.cpu(), v_ref),
+                           ("g", g_dev.cpu(), g.numpy())):
+        if not np.array_equal(got.numpy().view(np.uint32), np.asarray(ref, np.float32).view(np.uint32)):
+            print("MISMATCH", name, n); bad += 1
+print("HOST_MODE_OK" if bad == 0 else "HOST_MODE_BAD")
+"""
+
+
+@pytest.mark.parametrize("mode", ["hybrid", "pipe", "zc"])
+def test_host_paths_every_mode_bitexact(mode):
+    """Every host-buffer strategy (hybrid / copy pipeline / zero-copy) at 16 KB
+    stages (many stages, ragged tails): bit-identical to the oracle, device
+    copies included."""
+    import subprocess
+    env = dict(os.environ, FC_HOST_MODE=mode, FC_PIPE_CHUNK="4096")
+    r = subprocess.run([sys.executable, "-c", _HOST_MODE_CHILD, ROOT], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert "HOST_MODE_OK" in r.stdout, r.stdout + r.stderr
 
 
 @pytest.mark.parametrize("n", [7, 4105, 100_003])
