@@ -21,8 +21,11 @@ constexpr int TREE_T = kTreeThreads;              // threads per CTA (tree sched
 constexpr int FLAT_T = kFlatThreads;              // threads per CTA (FLAT / PS), one CTA per SM
 // float4 per thread per operand in flight in FLAT: enough remote bytes in flight
 // (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
-// (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*)
-#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : 2)
+// (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*).
+// p >= 7: U = 1 — U = 2 needs more than the 128 registers a 512-thread CTA
+// allows and spills 84-140 B/thread (ptxas -v), while U = 1 still keeps
+// 148 x 512 x 6..7 x 16 B = 7-8.5 MB in flight per GPU.
+#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : (P) <= 6 ? 2 : 1)
 constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
 constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
 static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");

@@ -30,7 +30,24 @@ struct KernelPick {
     bool flat;
 };
 
-static KernelPick pick_kernel(int sched, int arity, int p, int op) {
+// Tree schedules: the spill-free 1-CTA/SM build while the per-rank slice is
+// below 4M floats (16 MB), the 2-CTA/SM build above (measured, p = 2 and 4:
+// NiN forest/direct 65.5 vs 67.6 us, single_root/tree p=4 174 vs 190 us;
+// AlexNet forest/direct 0.377 vs 0.389 ms; profiles/r01_sweep_tree_launch_bounds_*,
+// scripts/gpu_tree_lb.sh).
+constexpr int64_t kTreeDenseSliceFloats = (int64_t)4 << 20;
+
+static int tree_ctas_per_sm(int p, int64_t n) {
+    static int force = -1;
+    if (force < 0) {
+        const char* e = getenv("FC_TREE_CTAS_PER_SM");
+        force = e ? atoi(e) : 0;
+    }
+    if (force == 1 || force == 2) return force;
+    return p > 0 && n / p >= kTreeDenseSliceFloats ? 2 : 1;
+}
+
+static KernelPick pick_kernel(int sched, int arity, int p, int op, int64_t n) {
     if (op == FC_OP_PS) arity = p;
     const bool bf16 = op == FC_OP_ALLREDUCE_SGD_BF16;  // always the FLAT executor
     const bool gather = op == FC_OP_ALLGATHER_OWNED;
@@ -39,8 +56,8 @@ static KernelPick pick_kernel(int sched, int arity, int p, int op) {
     if (gather) k.fn = allgather_kernel_for(p);
     else if (bf16) k.fn = flat_bf16_kernel_for(p, arity);
     else if (flat) k.fn = flat_kernel_for(p, arity);
-    else if (sched == FC_SCHED_SINGLE_ROOT) k.fn = single_root_kernel_for(p);
-    else k.fn = forest_kernel_for(p);
+    else if (sched == FC_SCHED_SINGLE_ROOT) k.fn = single_root_kernel_for(p, tree_ctas_per_sm(p, n));
+    else k.fn = forest_kernel_for(p, tree_ctas_per_sm(p, n));
     return k;
 }
 
@@ -50,7 +67,7 @@ static KernelPick pick_kernel(int sched, int arity, int p, int op) {
 // launch_bench.cu).  Tree schedules: as many 256-thread CTAs as fit (their
 // chunk pipeline wants more independent CTAs).  Virtual worlds share one GPU.
 int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
-    const KernelPick k = pick_kernel(sched, arity, p, op);
+    const KernelPick k = pick_kernel(sched, arity, p, op, n);
     if (!k.fn || p < 1) return 0;
     int occ = occupancy(k.fn, k.block);
     if (occ < 1) return 0;
@@ -78,7 +95,7 @@ int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
 
 cudaError_t launch_collective(const FcColl& c, int sched, int arity, bool virt, int grid_x,
                               cudaStream_t st) {
-    const KernelPick k = pick_kernel(sched, arity, c.p, c.op);
+    const KernelPick k = pick_kernel(sched, arity, c.p, c.op, c.n);
     if (!k.fn) return cudaErrorInvalidValue;
     dim3 grid(grid_x, virt ? c.p : 1), block(k.block);
     void* args[] = {(void*)&c};

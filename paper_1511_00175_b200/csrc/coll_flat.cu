@@ -178,8 +178,11 @@ const void* flat_kernel_for(int p, int arity) {
         case 2: return flat_kernel_u2(p, arity);
         case 4: return flat_kernel_u4(p, arity);
         default:
-            static_assert(FLAT_UNROLL(2) == 4 && FLAT_UNROLL(3) == 2 && FLAT_UNROLL(8) == 2, "table below");
-            return FLAT_UNROLL(p) == 4 ? flat_kernel_u4(p, arity) : flat_kernel_u2(p, arity);
+            switch (FLAT_UNROLL(p)) {
+                case 4: return flat_kernel_u4(p, arity);
+                case 2: return flat_kernel_u2(p, arity);
+                default: return flat_kernel_u1(p, arity);
+            }
     }
 }
 

@@ -9,8 +9,8 @@
 namespace fc {
 
 // ------------------------------------------------------------ FOREST -------
-template <int P>
-__global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
+template <int P, int MINB>
+__global__ void __launch_bounds__(TREE_T, MINB) forest_kernel(const FcColl c) {
     constexpr int M = (P >= 8) ? 3 : (P >= 4) ? 2 : (P >= 2) ? 1 : 0;
     static_assert((1 << M) == P, "forest needs a power-of-two world");
     const int rank = my_rank(c);
@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(TREE_T) forest_kernel(const FcColl c) {
 // ------------------------------------------------------------ SINGLE ROOT --
 // The paper's binomial tree rooted at rank 0: level l, rank r with
 // r % 2^(l+1) == 0 absorbs the whole partial of r + 2^l (if < p).
-template <int P>
-__global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
+template <int P, int MINB>
+__global__ void __launch_bounds__(TREE_T, MINB) single_root_kernel(const FcColl c) {
     const int rank = my_rank(c);
     const int G = gridDim.x, b = blockIdx.x;
     const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
@@ -198,24 +198,30 @@ __global__ void __launch_bounds__(TREE_T) single_root_kernel(const FcColl c) {
 }
 
 // ------------------------------------------------------------ kernel tables -
-template <int P>
+// Two register budgets per kernel (MINB = resident CTAs per SM the compiler
+// must allow): MINB = 1 lets a 256-thread CTA use ~160 registers with no
+// spills; MINB = 2 caps it at 128 and spills 8-76 B/thread (ptxas -v) but
+// doubles the CTAs in the chunk pipeline.  coll_dispatch.cu picks by slice size.
+template <int P, int MINB>
 static const void* forest_for() {
-    if constexpr ((P & (P - 1)) == 0) return (const void*)forest_kernel<P>;
+    if constexpr ((P & (P - 1)) == 0) return (const void*)forest_kernel<P, MINB>;
     else return nullptr;
 }
 
-const void* forest_kernel_for(int p) {
+const void* forest_kernel_for(int p, int ctas_per_sm) {
     switch (p) {
-#define FC_P(PP) case PP: return forest_for<PP>();
+#define FC_P(PP) case PP: return ctas_per_sm >= 2 ? forest_for<PP, 2>() : forest_for<PP, 1>();
         FC_P(2) FC_P(3) FC_P(4) FC_P(5) FC_P(6) FC_P(7) FC_P(8)
 #undef FC_P
     }
     return nullptr;
 }
 
-const void* single_root_kernel_for(int p) {
+const void* single_root_kernel_for(int p, int ctas_per_sm) {
     switch (p) {
-#define FC_P(PP) case PP: return (const void*)single_root_kernel<PP>;
+#define FC_P(PP)                                                                              \
+    case PP:                                                                                  \
+        return ctas_per_sm >= 2 ? (const void*)single_root_kernel<PP, 2> : (const void*)single_root_kernel<PP, 1>;
         FC_P(2) FC_P(3) FC_P(4) FC_P(5) FC_P(6) FC_P(7) FC_P(8)
 #undef FC_P
     }

@@ -50,8 +50,8 @@ constexpr int kFlatThreads = 512;  // threads per CTA, FLAT / PS / bf16 / all-ga
 const void* flat_kernel_for(int p, int arity);       // coll_flat.cu (also PS: arity = p)
 const void* flat_bf16_kernel_for(int p, int arity);  // coll_flat.cu
 const void* allgather_kernel_for(int p);             // coll_flat.cu
-const void* forest_kernel_for(int p);                // coll_tree.cu
-const void* single_root_kernel_for(int p);           // coll_tree.cu
+const void* forest_kernel_for(int p, int ctas_per_sm);       // coll_tree.cu (register budget
+const void* single_root_kernel_for(int p, int ctas_per_sm);  //   for 1 or 2 CTAs per SM)
 
 // Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
 __host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }

@@ -732,3 +732,24 @@ def test_virtual_rejects_non_symmetric_buffers():
             W.config("forest", "tree", 3)
     finally:
         W.close()
+
+
+# ----------------------------------------------------- kernel-selection knobs --
+@pytest.mark.skipif(os.environ.get("FC_KNOB_CHILD") == "1", reason="already inside a knob run")
+@pytest.mark.parametrize("knobs", [
+    {"FC_TREE_CTAS_PER_SM": "2"},                        # the 128-register tree builds (large-slice default)
+    {"FC_TREE_CTAS_PER_SM": "1"},                        # the spill-free tree builds (small-slice default)
+    {"FC_FLAT_UNROLL": "1"}, {"FC_FLAT_UNROLL": "2"}, {"FC_FLAT_UNROLL": "4"},  # every FLAT unroll build
+])
+def test_every_kernel_build_bitexact(knobs):
+    """The dispatcher picks among several builds of each executor (register
+    budget / unroll / CTAs per SM) by size; re-run the virtual-world parity
+    tests in a child process with each choice forced, so every build the
+    library can launch is checked bit for bit, not only the one the test
+    sizes happen to select."""
+    import subprocess
+    env = dict(os.environ, FC_KNOB_CHILD="1", **knobs)
+    sel = "test_virtual_fused_bitexact or test_virtual_tree_allreduce_bitexact or test_virtual_ps_bitexact"
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu", "-k", sel,
+                        "-p", "no:cacheprovider"], env=env, cwd=ROOT, capture_output=True, text=True, timeout=1800)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
