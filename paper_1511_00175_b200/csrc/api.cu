@@ -116,6 +116,21 @@ static float inv_batch(int64_t batch) {
     return one / b;
 }
 
+// Exit protocol of the collectives (coll_common.cuh): rank-level (default: the
+// last CTA per GPU does one sys fence + stamp exchange) or, with FC_EXIT=cta,
+// the per-CTA exit barrier.  Measured (scripts/gpu_exit_sweep.sh,
+// profiles/r01_sweep_exit_*): 1-4 us faster per call up to NiN size, equal at
+// AlexNet size.  Part of the call signature, so ranks that disagree fail with
+// FC_ERR_MISMATCH at entry instead of waiting on stamps that never come.
+static int exit_mode() {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("FC_EXIT");
+        m = (e && strcmp(e, "cta") == 0) ? 0 : 1;
+    }
+    return m;
+}
+
 extern "C" {
 
 const char* firecaffe_version(void) { return FC_VERSION_STR; }
@@ -445,9 +460,12 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         mix(&c.wd, sizeof c.wd);
         mix(&c.inv_b, sizeof c.inv_b);
         mix(&seg_hash, sizeof seg_hash);
+        const int rx = exit_mode();
+        mix(&rx, sizeof rx);
         c.sig = h;
     }
     c.op = op;
+    c.rank_exit = exit_mode();
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;

@@ -143,6 +143,70 @@ static __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
     return __syncthreads_and(good) != 0;
 }
 
+// Rank-level exit (c.rank_exit = 1): instead of an all-to-all barrier per CTA
+// (every CTA paying a sys-scope fence; the fence gets slower the more CTAs
+// issue it), every CTA orders its writes — local and peer — with a gpu-scope
+// fence and arrives on the call's CTA counter (ctl[1]); the LAST CTA to arrive
+// on this GPU makes all of them visible system-wide with ONE sys fence, stamps
+// every peer's exit word and waits for every peer's stamp (written by that
+// peer's last CTA after all of ITS CTAs arrived).  When the kernel ends, every
+// store any peer made into this rank's heap has landed.  Memory-model chain
+// (PTX causality order is transitive): CTA stores -> fence.gpu + counter
+// increment -> last CTA's increment + fence.gpu (same GPU) -> fence.sys +
+// stamp -> the peer's acquire.sys of the stamp.  The other CTAs leave at once.
+// Then the epoch advances as in epoch_end.  Virtual worlds: the last CTA of
+// the whole grid already follows every rank's CTAs, no stamps needed.
+static __device__ __noinline__ void exit_rank(const FcColl& c, int rank) {
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    __threadfence();
+    const uint32_t total = gridDim.x * gridDim.y;
+    const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
+    if (done != total) return;
+    __threadfence();
+    if (c.rank >= 0) {
+        const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
+        fence_sys();
+        for (int q = 0; q < c.p; ++q)
+            if (q != rank) st_relaxed_sys64(bar_flag(c, q, 1, 0, rank), stamp);
+        const uint64_t t0 = globaltimer();
+        for (int q = 0; q < c.p; ++q) {
+            if (q == rank) continue;
+            const uint64_t* f = bar_flag(c, rank, 1, 0, q);
+            uint32_t spins = 0;
+            bool good = true;
+            while (!reached((uint32_t)ld_relaxed_sys64(f), s_epoch)) {
+                if ((++spins & 63u) == 0) {
+                    if (*(volatile int*)c.status != FC_OK) { good = false; break; }
+                    if (globaltimer() - t0 > c.timeout_ns) {
+                        atomicCAS(c.status, FC_OK, FC_ERR_TIMEOUT);
+                        good = false;
+                        break;
+                    }
+                }
+            }
+            if (!good) break;
+            (void)ld_acquire_sys64(f);
+        }
+    }
+    c.ctl[1] = 0u;
+    __threadfence();
+    atomicExch(c.ctl, s_epoch);
+}
+
+// End of a collective whose data phase may have written into peers' heaps:
+// the exit barrier (per CTA, or per rank with c.rank_exit), then the epoch.
+__device__ __forceinline__ void finish_call(const FcColl& c, int rank) {
+    if (c.rank_exit) {
+        exit_rank(c, rank);
+        trace(c, 3);
+        return;
+    }
+    cta_barrier(c, rank, 1);
+    trace(c, 3);
+    epoch_end(c);
+}
+
 // One thread waits for a flag; the CTA learns the outcome.
 __device__ __forceinline__ bool wait_one(const FcColl& c, const uint32_t* f) {
     bool good = true;

@@ -103,9 +103,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
         }
     }
     trace(c, 2);
-    cta_barrier(c, rank, 1);
-    trace(c, 3);
-    epoch_end(c);
+    finish_call(c, rank);
 }
 
 // ------------------------------------------------------------ ALLGATHER ----
@@ -156,9 +154,7 @@ __global__ void __launch_bounds__(FLAT_T) allgather_kernel(const FcColl c) {
         }
     }
     trace(c, 2);
-    cta_barrier(c, rank, 1);
-    trace(c, 3);
-    epoch_end(c);
+    finish_call(c, rank);
 }
 
 // ------------------------------------------------------------ kernel tables -

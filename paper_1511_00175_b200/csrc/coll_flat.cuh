@@ -166,8 +166,12 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     // finished results (release after local stores only); then this CTA copies
     // the matching elements of every peer's slice (the ones that peer's CTA
     // with the same index produced) and the kernel ends with no remote writes.
+    if (!pull) {
+        finish_call(c, rank);
+        return;
+    }
     const bool ok2 = cta_barrier(c, rank, 1);
-    if (pull && ok && ok2) pull_results<P, U>(c, rank);
+    if (ok && ok2) pull_results<P, U>(c, rank);
     trace(c, 3);
     epoch_end(c);
 }

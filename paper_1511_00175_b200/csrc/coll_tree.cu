@@ -96,7 +96,8 @@ __global__ void __launch_bounds__(TREE_T, MINB) forest_kernel(const FcColl c) {
                 if (!wait_one(c, av_flag(c, rank, cc))) break;
         }
     } else {
-        cta_barrier(c, rank, 1);
+        finish_call(c, rank);
+        return;
     }
     trace(c, 3);
     epoch_end(c);
@@ -191,7 +192,8 @@ __global__ void __launch_bounds__(TREE_T, MINB) single_root_kernel(const FcColl 
         if (ok && pend) publish_batch(c, cc_last, G, pend, stamp);
       }
     } else {
-        cta_barrier(c, rank, 1);
+        finish_call(c, rank);
+        return;
     }
     trace(c, 3);
     epoch_end(c);

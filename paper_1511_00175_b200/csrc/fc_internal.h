@@ -67,6 +67,7 @@ struct FcColl {
     int owner_single_root;  // ownership of the single-root schedule (rank 0 owns all)
     int64_t bar_words, red_words, max_chunks;
     uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]
+    int rank_exit;     // 1: rank-level exit (one sys fence per GPU), 0: per-CTA exit barrier
 };
 
 #define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--nccl", action="store_true")
     ap.add_argument("--sleep", type=int, default=40000, help="GPU cycles of delay after the rendezvous")
+    ap.add_argument("--max-ctas", default="0", help="comma list of per-rank CTA caps (0 = library default)")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -63,9 +64,10 @@ def main():
     for op in args.ops.split(","):
         for n in sizes:
             variants = [("ps", "-")] if op == "ps" else (scheds + ([("nccl", "-")] if args.nccl else []))
-            for sched, bcast in variants:
+            for sched, bcast, cap in [(a, b, int(c)) for a, b in variants for c in args.max_ctas.split(",")]:
                 if sched not in ("ps", "nccl"):
                     W.config(sched, bcast, 2)
+                W.set_max_ctas(cap)
                 ms, spans, ph = [], [], [[], [], []]
                 for it in range(args.iters + 3):
                     grad[:n].copy_(g0[:n])
@@ -102,7 +104,8 @@ def main():
                 dist.all_reduce(tot, op=dist.ReduceOp.MAX)
                 if rank == 0:
                     t_ms = tot.item()
-                    rec = {"p": p, "op": op, "sched": sched, "bcast": bcast, "n": n, "ms": round(t_ms, 4),
+                    rec = {"p": p, "op": op, "sched": sched, "bcast": bcast, "n": n, "max_ctas": cap,
+                           "ms": round(t_ms, 4),
                            "busbw_gbs": round(4 * n / (t_ms * 1e-3) / 1e9 * 2 * (p - 1) / p, 1)}
                     if spans:
                         rec.update(span_us=round(statistics.median(spans), 2),

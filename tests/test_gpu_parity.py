@@ -740,6 +740,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_TREE_CTAS_PER_SM": "2"},                        # the 128-register tree builds (large-slice default)
     {"FC_TREE_CTAS_PER_SM": "1"},                        # the spill-free tree builds (small-slice default)
     {"FC_FLAT_UNROLL": "1"}, {"FC_FLAT_UNROLL": "2"}, {"FC_FLAT_UNROLL": "4"},  # every FLAT unroll build
+    {"FC_EXIT": "rank"}, {"FC_EXIT": "cta"},            # both exit protocols (coll_common.cuh)
 ])
 def test_every_kernel_build_bitexact(knobs):
     """The dispatcher picks among several builds of each executor (register
@@ -749,7 +750,9 @@ def test_every_kernel_build_bitexact(knobs):
     sizes happen to select."""
     import subprocess
     env = dict(os.environ, FC_KNOB_CHILD="1", **knobs)
-    sel = "test_virtual_fused_bitexact or test_virtual_tree_allreduce_bitexact or test_virtual_ps_bitexact"
+    sel = ("test_virtual_fused_bitexact or test_virtual_tree_allreduce_bitexact or test_virtual_ps_bitexact"
+           " or test_back_to_back_steps_without_host_sync or test_virtual_fused_bf16_bitexact"
+           " or test_allgather_owned_momentum_checkpoint")
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu", "-k", sel,
                         "-p", "no:cacheprovider"], env=env, cwd=ROOT, capture_output=True, text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
