@@ -262,7 +262,13 @@ fc_status firecaffe_tree_allreduce_sgd_bf16(float* w, uint16_t* grad, float* mom
  *   `stream`; later work on `stream` sees every copy complete.  Not re-entrant
  *   across host threads on the same device.
  * firecaffe_tree_allreduce_sgd_host: H2D into the symmetric grad, the fused
- *   collective, D2H of the updated weights, on `stream`.
+ *   collective, D2H of the updated weights.  With the FLAT executor (push
+ *   broadcast) and n >= S*p*4096 it runs as an S-stage pipeline on internal
+ *   streams (S = FC_HOST_STAGES, default 4): stage k's H2D || stage k-1's
+ *   collective || stage k-2's D2H, stage k covering window k of every owner's
+ *   slice, so w, mom (owned slice) and grad end bitwise as after one full
+ *   call.  Otherwise serial on `stream`.  Either way ordered after prior work
+ *   on `stream`, and later work on `stream` sees the weights on the host.
  * segs may be NULL (uniform multipliers).  Errors as the device versions, plus
  * FC_ERR_INVALID_ARG for host buffers that are not page-locked. */
 fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float* grad_host,

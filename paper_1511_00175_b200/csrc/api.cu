@@ -13,6 +13,7 @@
 #include "fc_launch.h"
 
 #define FC_VERSION_STR "firecaffe-b200 0.1.0 sm_100a"
+#define FC_HOST_MAX_STAGES 16
 
 struct fc_segments {
     int nseg;
@@ -44,6 +45,10 @@ struct fc_world {
     int64_t trace_cap;
     int last_grid;
     int max_ctas;  // 0 = automatic
+    // staged host entry point (firecaffe_tree_allreduce_sgd_host), created on first use
+    bool hp_ready;
+    cudaStream_t hp_s[3];  // H2D, collective, D2H
+    cudaEvent_t hp_start, hp_h2d[FC_HOST_MAX_STAGES], hp_coll[FC_HOST_MAX_STAGES];
 };
 
 namespace fc {
@@ -282,6 +287,14 @@ fc_status firecaffe_world_destroy(fc_world* w) {
         if (w->opened[q] && cudaIpcCloseMemHandle(w->peer[q]) != cudaSuccess) st = FC_ERR_CUDA;
     if (w->d_status) cudaFree(w->d_status);
     if (w->d_ctl) cudaFree(w->d_ctl);
+    if (w->hp_ready) {
+        for (int i = 0; i < 3; ++i) cudaStreamDestroy(w->hp_s[i]);
+        cudaEventDestroy(w->hp_start);
+        for (int i = 0; i < FC_HOST_MAX_STAGES; ++i) {
+            cudaEventDestroy(w->hp_h2d[i]);
+            cudaEventDestroy(w->hp_coll[i]);
+        }
+    }
     delete w;
     return st;
 }
@@ -408,7 +421,7 @@ static int64_t heap_offset(const fc_world* w, const void* p, int64_t n) {
 
 static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* mom, int64_t n,
                             float lr, float mu, float wd, int64_t batch,
-                            const fc_segments* segs, void* stream) {
+                            const fc_segments* segs, void* stream, int win_k = 0, int win_s = 1) {
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
     if (cur != w->device) return FC_ERR_MISMATCH;
@@ -462,10 +475,14 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         mix(&seg_hash, sizeof seg_hash);
         const int rx = exit_mode();
         mix(&rx, sizeof rx);
+        mix(&win_k, sizeof win_k);
+        mix(&win_s, sizeof win_s);
         c.sig = h;
     }
     c.op = op;
     c.rank_exit = exit_mode();
+    c.win_k = win_k;
+    c.win_s = win_s;
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;
@@ -709,6 +726,50 @@ fc_status firecaffe_sgd_step_host(float* w, float* grad, float* mom, const float
     return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 
+// Stages of the pipelined host entry point (FC_HOST_STAGES, default 4; 1 = serial).
+static int host_stages() {
+    static int s = -1;
+    if (s < 0) {
+        const char* e = getenv("FC_HOST_STAGES");
+        s = e ? atoi(e) : 4;
+        if (s < 1) s = 1;
+        if (s > FC_HOST_MAX_STAGES) s = FC_HOST_MAX_STAGES;
+    }
+    return s;
+}
+
+static fc_status host_pipe_ready(fc_world* w) {
+    if (w->hp_ready) return FC_OK;
+    for (int i = 0; i < 3; ++i)
+        if (cudaStreamCreateWithFlags(&w->hp_s[i], cudaStreamNonBlocking) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaEventCreateWithFlags(&w->hp_start, cudaEventDisableTiming) != cudaSuccess) return FC_ERR_CUDA;
+    for (int i = 0; i < FC_HOST_MAX_STAGES; ++i)
+        if (cudaEventCreateWithFlags(&w->hp_h2d[i], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&w->hp_coll[i], cudaEventDisableTiming) != cudaSuccess)
+            return FC_ERR_CUDA;
+    w->hp_ready = true;
+    return FC_OK;
+}
+
+// Elements [x, y) that stage k of s of the FLAT collective processes in owner
+// r's slice (the kernel's window_range on float4 units; the n % 4 tail rides
+// with the last stage).
+static void stage_range(int r, int p, int64_t n, int k, int s, int64_t* x, int64_t* y) {
+    const int64_t nch = (n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    int64_t c0, c1;
+    owned_chunks(r, p, nch, false, &c0, &c1);
+    const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+    const int64_t e1 = c1 * FC_CHUNK_FLOATS < n ? c1 * FC_CHUNK_FLOATS : n;
+    if (e1 <= e0) {
+        *x = *y = e0;
+        return;
+    }
+    int64_t a, b;
+    window_range(e0 / 4, e1 / 4, k, s, &a, &b);
+    *x = 4 * a;
+    *y = k == s - 1 ? e1 : 4 * b;
+}
+
 fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
                                             const float* grad_host, float* w_host, int64_t n,
                                             float lr, float mu, float wd, int64_t batch,
@@ -722,15 +783,67 @@ fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
     if (n == 0) return FC_OK;
     if (!grad_host || !w_host || !pinned_host(grad_host) || !pinned_host(w_host))
         return FC_ERR_INVALID_ARG;
-    if (check_vec(grad, n) || check_vec(w, n)) return FC_ERR_INVALID_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemcpyAsync(grad, grad_host, n * 4, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return FC_ERR_CUDA;
-    fc_status st = fused_impl(w, grad, mom, n, lr, mu, wd, batch, segs, world, stream);
+    fc_status st = check_hyper(lr, mu, wd, batch);
     if (st != FC_OK) return st;
-    if (cudaMemcpyAsync(w_host, w, n * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-        return FC_ERR_CUDA;
-    return FC_OK;
+    if (check_vec(grad, n) || check_vec(w, n) || check_vec(mom, n)) return FC_ERR_INVALID_ARG;
+    const int64_t bytes = n * 4;
+    if (overlap(w, grad, bytes) || overlap(w, mom, bytes) || overlap(grad, mom, bytes) ||
+        overlap(grad_host, w_host, bytes))
+        return FC_ERR_INVALID_ARG;
+    FcSegs sd;
+    if ((st = check_segs(segs, n, &sd)) != FC_OK) return st;
+    if (heap_offset(world, grad, n) < 0 || heap_offset(world, w, n) < 0) return FC_ERR_NOT_SYMMETRIC;
+    cudaStream_t user = (cudaStream_t)stream;
+    const int S = host_stages();
+    const int p = world->p;
+    const bool staged = S > 1 && world->sched == FC_SCHED_FLAT && world->bcast != FC_BCAST_PULL &&
+                        n >= (int64_t)S * p * FC_CHUNK_FLOATS;
+    if (!staged) {  // serial: H2D, the fused collective, D2H on the caller's stream
+        if (cudaMemcpyAsync(grad, grad_host, bytes, cudaMemcpyHostToDevice, user) != cudaSuccess)
+            return FC_ERR_CUDA;
+        st = fused_impl(w, grad, mom, n, lr, mu, wd, batch, segs, world, stream);
+        if (st != FC_OK) return st;
+        if (cudaMemcpyAsync(w_host, w, bytes, cudaMemcpyDeviceToHost, user) != cudaSuccess)
+            return FC_ERR_CUDA;
+        return FC_OK;
+    }
+    // Staged (S stages, three internal streams): stage k's gradient windows come
+    // in on the H2D copy engine while stage k-1's collective runs over NVLink and
+    // stage k-2's weights go out on the D2H copy engine.  Stage k of the FLAT
+    // collective covers window k of EVERY owner's slice, so the momentum
+    // ownership and the bits equal one full call (tested).
+    if ((st = host_pipe_ready(world)) != FC_OK) return st;
+    cudaStream_t* hs = world->hp_s;
+    if (cudaEventRecord(world->hp_start, user) != cudaSuccess) return FC_ERR_CUDA;
+    for (int i = 0; i < 3; ++i)
+        if (cudaStreamWaitEvent(hs[i], world->hp_start, 0) != cudaSuccess) return FC_ERR_CUDA;
+    for (int k = 0; k < S; ++k) {
+        for (int r = 0; r < p; ++r) {
+            int64_t x, y;
+            stage_range(r, p, n, k, S, &x, &y);
+            if (y > x && cudaMemcpyAsync(grad + x, grad_host + x, (y - x) * 4, cudaMemcpyHostToDevice,
+                                         hs[0]) != cudaSuccess)
+                return FC_ERR_CUDA;
+        }
+        if (cudaEventRecord(world->hp_h2d[k], hs[0]) != cudaSuccess ||
+            cudaStreamWaitEvent(hs[1], world->hp_h2d[k], 0) != cudaSuccess)
+            return FC_ERR_CUDA;
+        st = collective(world, FC_OP_ALLREDUCE_SGD, w, grad, mom, n, lr, mu, wd, batch, segs, hs[1], k, S);
+        if (st != FC_OK) return st;
+        if (cudaEventRecord(world->hp_coll[k], hs[1]) != cudaSuccess ||
+            cudaStreamWaitEvent(hs[2], world->hp_coll[k], 0) != cudaSuccess)
+            return FC_ERR_CUDA;
+        for (int r = 0; r < p; ++r) {
+            int64_t x, y;
+            stage_range(r, p, n, k, S, &x, &y);
+            if (y > x &&
+                cudaMemcpyAsync(w_host + x, w + x, (y - x) * 4, cudaMemcpyDeviceToHost, hs[2]) != cudaSuccess)
+                return FC_ERR_CUDA;
+        }
+    }
+    // the caller's stream continues after the last weights are on the host
+    if (cudaEventRecord(world->hp_start, hs[2]) != cudaSuccess) return FC_ERR_CUDA;
+    return cudaStreamWaitEvent(user, world->hp_start, 0) == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 
 // The paper's learning-rate schedules, in double, one

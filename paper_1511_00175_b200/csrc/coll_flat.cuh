@@ -83,12 +83,17 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
         if (e1 > e0) {
             // push broadcast: results go to every rank's buffer now; pull broadcast:
             // only to the own buffer, the peers fetch them after the publish barrier
-            const int64_t i0 = e0 / 4, i1 = e1 / 4;
+            const int64_t i1 = e1 / 4;
             const int64_t T = FLAT_T;
+            // stage window (c.win_s > 1, the pipelined host entry point): only
+            // window win_k of win_s of this rank's slice; the n % 4 tail goes with
+            // the last window
+            int64_t i0 = e0 / 4, ce = i1;
+            if (c.win_s > 1) window_range(e0 / 4, i1, c.win_k, c.win_s, &i0, &ce);
+            const bool tail_here = c.win_s <= 1 || c.win_k == c.win_s - 1;
             // grid-stride: all CTAs sweep the slice in lockstep, so at any moment the
             // GPU's remote reads fall in one few-MB window of each peer's heap (a
             // contiguous range per CTA measured ~10% slower: 444 scattered streams)
-            const int64_t ce = i1;
             const int64_t stride = (int64_t)gridDim.x * T * U;
             for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < ce;
                  base += stride) {
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
             }
             // trailing n % 4 elements of the last slice
             const int rem = (int)(e1 - 4 * i1);
-            if (blockIdx.x == 0 && (int)threadIdx.x < rem) {
+            if (tail_here && blockIdx.x == 0 && (int)threadIdx.x < rem) {
                 const int64_t e = 4 * i1 + threadIdx.x;
                 float xs[P];
 #pragma unroll

@@ -53,6 +53,15 @@ const void* allgather_kernel_for(int p);             // coll_flat.cu
 const void* forest_kernel_for(int p, int ctas_per_sm);       // coll_tree.cu (register budget
 const void* single_root_kernel_for(int p, int ctas_per_sm);  //   for 1 or 2 CTAs per SM)
 
+// Window k of s of the index range [a, b): [a + L*k/s, a + L*(k+1)/s), L = b - a
+// (host + device: the pipelined host entry point and the FLAT kernel agree on it).
+__host__ __device__ inline void window_range(int64_t a, int64_t b, int k, int s, int64_t* wa,
+                                             int64_t* wb) {
+    const int64_t L = b - a;
+    *wa = a + L * k / s;
+    *wb = a + L * (k + 1) / s;
+}
+
 // Owned chunk range [c0, c1) (in FC_CHUNK_FLOATS units) of `rank` (host + device).
 __host__ __device__ inline bool is_pow2(int p) { return p > 0 && (p & (p - 1)) == 0; }
 __host__ __device__ inline void owned_chunks(int rank, int p, int64_t n_chunks, bool single_root,

@@ -111,6 +111,23 @@ def main():
         torch.cuda.synchronize()
         if not np.array_equal(w_host.numpy().view(np.uint32), w_ref.view(np.uint32)):
             fails.append(f"host entry w n={n}")
+        if not np.array_equal(bits(w[:n]), w_ref.view(np.uint32)):
+            fails.append(f"host entry device w n={n}")
+        b, e = W.owned_range(rank, n)  # staged or not: the ownership of one full call
+        if not np.array_equal(bits(mom[b:e]), v_ref[b:e].view(np.uint32)):
+            fails.append(f"host entry mom n={n}")
+        if not np.array_equal(bits(grad[:n]), g_all[rank].numpy().view(np.uint32)):
+            fails.append(f"host entry grad copy n={n}")
+        # the same with per-blob multipliers
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        w_host.fill_(float("nan"))
+        fc.firecaffe_tree_allreduce_sgd_host(w, grad, mom, g_host, w_host, world=W, n=n, segs=segs, **HP)
+        torch.cuda.synchronize()
+        if not np.array_equal(w_host.numpy().view(np.uint32), ws_ref.view(np.uint32)):
+            fails.append(f"host entry segments w n={n}")
+        if not np.array_equal(bits(mom[b:e]), vs_ref[b:e].view(np.uint32)):
+            fails.append(f"host entry segments mom n={n}")
     # back-to-back fused steps across real GPUs, no host synchronisation between
     # them (each rank refreshes its own gradient with a stream-ordered copy)
     n = sizes[-1]
