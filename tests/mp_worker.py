@@ -149,6 +149,49 @@ def main():
             wr, vr = oracle.fused_step(gsteps[s].numpy(), wr, vr, **HP)
         if not np.array_equal(bits(w[:n]), wr.view(np.uint32)):
             fails.append(f"back-to-back {sched}/{bcast}")
+    # stress: many back-to-back collectives (random op, executor and size, the
+    # same sequence on every rank), no host synchronisation and no barrier in
+    # between, so rank skew accumulates freely; each result is compared on the
+    # device (stream-ordered) with oracle results computed once per (op, n)
+    iters = int(os.environ.get("FC_MP_STRESS", "200"))
+    if iters > 0:
+        rng = np.random.default_rng(4242)  # same stream of choices on every rank
+        stress_sizes = [1, 4, 4097, 3 * 4096 + 5, 65536 + 3, 200_003]
+        plans = []
+        exp = {}
+        for n in stress_sizes:
+            ga = fc_inputs.grads(n, p, seed=7000 + n)
+            w0s, v0s = fc_inputs.weights(n, seed=71), fc_inputs.momentum(n, seed=72)
+            S = oracle.tree_sum(ga.numpy(), 2)
+            wr, vr = oracle.sgd(w0s.numpy(), v0s.numpy(), S, **HP)
+            exp[n] = dict(g=ga[rank].to(dev), w0=w0s.to(dev), v0=v0s.to(dev), S=torch.from_numpy(S).to(dev),
+                          ps=torch.from_numpy(oracle.ps_sum(ga.numpy())).to(dev), w=torch.from_numpy(wr).to(dev),
+                          v=torch.from_numpy(vr).to(dev))
+        bad = torch.zeros((), dtype=torch.int64, device=dev)
+        cfgs = [c for c in scheds if not (c[0] == "forest" and (p & (p - 1)))]
+        for it in range(iters):
+            n = stress_sizes[rng.integers(len(stress_sizes))]
+            op = ("fused", "allreduce", "ps")[rng.integers(3)]
+            sched, bcast = cfgs[rng.integers(len(cfgs))]
+            W.config(sched, bcast, 2)
+            e = exp[n]
+            grad[:n].copy_(e["g"])
+            if op == "fused":
+                w[:n].copy_(e["w0"])
+                mom[:n].copy_(e["v0"])
+                fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, n=n, **HP)
+                b, e_ = W.owned_range(rank, n)
+                bad += (w[:n].view(torch.int32) != e["w"].view(torch.int32)).sum()
+                bad += (mom[b:e_].view(torch.int32) != e["v"][b:e_].view(torch.int32)).sum()
+            elif op == "allreduce":
+                fc.firecaffe_tree_allreduce(grad, W, n=n)
+                bad += (grad[:n].view(torch.int32) != e["S"].view(torch.int32)).sum()
+            else:
+                fc.firecaffe_ps_allreduce(grad, W, n=n)
+                bad += (grad[:n].view(torch.int32) != e["ps"].view(torch.int32)).sum()
+        torch.cuda.synchronize()
+        if bad.item() != 0:
+            fails.append(f"stress: {bad.item()} mismatched elements over {iters} calls")
     st = W.poll()
     if st != 0:
         fails.append(f"device status {st}")

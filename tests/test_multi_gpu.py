@@ -40,7 +40,7 @@ def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
         pytest.skip(f"needs {nproc} GPUs")
     env = dict(os.environ, FC_MP_TIMEOUT="5", OMP_NUM_THREADS="1", FC_MP_TIMEOUT_TEST="0", FC_TREE_CTAS_PER_SM="2",
                FC_FLAT_UNROLL="1", FC_FLAT_CTAS_PER_SM="2", FC_LAUNCH="coop", FC_EXIT=exit_mode,
-               FC_HOST_STAGES="3")
+               FC_HOST_STAGES="3", FC_MP_STRESS="1500")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={29610 + nproc}", os.path.join(ROOT, "tests", "mp_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
