@@ -468,6 +468,10 @@ def main():
                 # this traffic's own measured ceiling (both directions loaded, SM loads+stores;
                 # scripts/nvlink_bench.cu, profiles/r01_nvlink_bench_sm.txt)
                 "frac_of_measured_bidirectional_690": round(achieved / 690.0, 4)}
+        if roof["traffic"] is None:
+            roof["traffic_note"] = ("ncu cannot replay a cross-GPU kernel (the peers' flags never arrive); the same "
+                                    "kernel in a virtual world reads exactly the algorithmic bytes from DRAM "
+                                    "(profiles/r01_ncu_flat_virtual_p4_nin.json)")
 
     # ---- baselines on the same buffers (context: PS, paper's single-root tree, NCCL, torch)
     baselines = {}
