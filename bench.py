@@ -35,6 +35,26 @@ METRIC = "tree-allreduce+SGD ms/iter and algo GB/s at 1/2/4/8 B200, % of NVLink/
 GUIDE_NVLINK_PEER_GBS = 770.0  # B200_PROFILING.md: measured peer copy, per direction per GPU
 NVLINK_NOMINAL_GBS = 900.0
 
+# The JSON line is the only thing this script writes to stdout: native
+# libraries (NCCL prints "NCCL version ..." at init on some boxes) write to
+# file descriptor 1 directly, so fd 1 is pointed at stderr and the JSON goes to
+# a private duplicate of the original stdout.
+_JSON_OUT = None
+
+
+def _claim_stdout():
+    global _JSON_OUT
+    if _JSON_OUT is None:
+        sys.stdout.flush()
+        _JSON_OUT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    _claim_stdout()
+    _JSON_OUT.write(json.dumps(line) + "\n")
+    _JSON_OUT.flush()
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -293,7 +313,7 @@ def run_reference(args):
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -316,7 +336,7 @@ def main():
     N = world
     if args.gpus != N:
         if N == 1 and args.gpus > 1:
-            print(json.dumps({"error": "run N>1 under torchrun"}), flush=True)
+            emit({"error": "run N>1 under torchrun"})
             return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -564,7 +584,7 @@ def main():
             "baselines_ms_per_step": baselines,
             "wall_s_timed_region": round(wall, 3),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if N > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -625,4 +645,5 @@ def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, rese
 
 
 if __name__ == "__main__":
+    _claim_stdout()
     sys.exit(main())
