@@ -31,6 +31,9 @@
  *     MPI/NCCL convention).  Their `grad`, `w` (and, for a virtual world,
  *     `mom`) must lie inside the world's heap at the SAME byte offset on every
  *     rank (symmetric allocation), at or after firecaffe_heap_reserved_bytes().
+ *     Ranks whose calls differ in any of these (op, n, executor, hyper-
+ *     parameters, blob table, buffer offsets) all fail with a sticky
+ *     FC_ERR_MISMATCH before any data moves.
  *   - Every device-side call (all but the *_host entry points' host checks) can
  *     be captured in a CUDA graph and replayed: kernel arguments do not change
  *     between calls (the collectives' call counter lives in device memory).
@@ -53,7 +56,9 @@ typedef enum {
     FC_OK = 0,
     FC_ERR_INVALID_ARG = 1,   /* null/misaligned pointer, n < 0, lr <= 0, mu not in [0,1), wd < 0, batch < 1, overlap */
     FC_ERR_NOT_SYMMETRIC = 2, /* a collective buffer is outside the heap or inside its reserved prefix */
-    FC_ERR_MISMATCH = 3,      /* world/device mismatch (e.g. called on another device) */
+    FC_ERR_MISMATCH = 3,      /* world/device mismatch (called on another device), or, sticky from
+                                 firecaffe_world_poll, ranks that made different collective calls
+                                 (op, n, executor, hyper-parameters, blob table, buffer offsets) */
     FC_ERR_TIMEOUT = 4,       /* a peer did not arrive within the world's timeout (sticky) */
     FC_ERR_CUDA = 5,          /* a CUDA runtime call failed */
     FC_ERR_UNSUPPORTED = 6    /* schedule/arity not available for this world size */

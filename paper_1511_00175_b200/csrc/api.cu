@@ -477,6 +477,11 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         mix(&rx, sizeof rx);
         mix(&win_k, sizeof win_k);
         mix(&win_s, sizeof win_s);
+        // the buffers' heap offsets: a peer's buffer is addressed at THIS
+        // rank's offset, so ranks that disagree must fail, not read garbage
+        mix(&c.off_grad, sizeof c.off_grad);
+        mix(&c.off_w, sizeof c.off_w);
+        mix(&c.off_mom, sizeof c.off_mom);
         c.sig = h;
     }
     c.op = op;

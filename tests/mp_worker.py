@@ -215,6 +215,20 @@ def main():
         fails.append(f"expected FC_ERR_MISMATCH, got {st2}")
     if not bool((g2 == float(rank + 1)).all().item()):
         fails.append("mismatched call modified data")
+    # ranks disagree on where the buffer sits in the heap (same n): peers would
+    # be read at the wrong offset, so this must fail the same way
+    W3 = fc.World.create(heap_bytes_for(4096 + 4096), timeout_s=5.0)
+    g3 = W3.alloc(4096)
+    g3.fill_(float(rank + 1))
+    torch.cuda.synchronize()
+    dist.barrier()
+    fc.firecaffe_tree_allreduce(g3[4 * rank:], W3, n=1000)
+    st3 = W3.poll()
+    if st3 != 3:
+        fails.append(f"offset mismatch: expected FC_ERR_MISMATCH, got {st3}")
+    if not bool((g3 == float(rank + 1)).all().item()):
+        fails.append("offset-mismatched call modified data")
+    W3.close()
     dist.barrier()
     nf = torch.tensor([len(fails)], device=dev)
     dist.all_reduce(nf)
