@@ -288,10 +288,14 @@ fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
 /* ------------------------------------------------ learning-rate schedules
  * The paper's schedules (R21): FIXED; STEP gamma^floor(iter/stepsize);
  * MULTISTEP gamma^#{steps[k] <= iter} ("reduce this by a factor of 10x twice",
- * P:407); POLY (1 - iter/max_iter)^power (power 0.5).  Evaluated in
- * double and rounded once to fp32; host-only.  Returns -1 for invalid input
- * (iter < 0, base_lr <= 0, stepsize < 1 for STEP, iter > max_iter for POLY,
- * nsteps outside 0..FC_LR_MAX_STEPS). */
+ * P:407); POLY (1 - iter/max_iter)^power (power 0.5).  The factor
+ * is evaluated in double (gamma^k by binary powering: k = 1, 2 give gamma and
+ * fl(gamma^2); power 0.5 as sqrt, power 1 exactly, other powers via pow), then
+ * lr = fl32(base_lr * factor).  firecaffe_lr_at evaluates it on the host;
+ * the *_sched entry points below evaluate the same arithmetic on the device.
+ * firecaffe_lr_at returns -1 for invalid input (iter < 0, base_lr <= 0 or not
+ * finite, stepsize < 1 for STEP, iter > max_iter or max_iter < 1 for POLY,
+ * nsteps outside 0..FC_LR_MAX_STEPS, non-finite gamma / power). */
 typedef enum { FC_LR_FIXED = 0, FC_LR_STEP = 1, FC_LR_MULTISTEP = 2, FC_LR_POLY = 3 } fc_lr_policy;
 #define FC_LR_MAX_STEPS 16
 typedef struct {
@@ -305,6 +309,37 @@ typedef struct {
     int64_t steps[FC_LR_MAX_STEPS];
 } fc_lr_schedule;
 float firecaffe_lr_at(const fc_lr_schedule* sched, int64_t iter);
+
+/* On-device schedules ("computed on device from an iteration
+ * counter, so the step needs no host sync").  An fc_lr_state is a device copy
+ * of the schedule plus an iteration counter, on the device current at
+ * creation.  firecaffe_sgd_step_sched / firecaffe_tree_allreduce_sgd_sched
+ * are firecaffe_sgd_step / firecaffe_tree_allreduce_sgd with lr =
+ * firecaffe_lr_at(sched, iter) computed by the kernel from the counter, which
+ * the same kernel then advances by one (stream-ordered): a captured CUDA
+ * graph replays the training step with the schedule moving on, no host
+ * involvement.  POLY at iter >= max_iter gives lr = 0.  A call that enqueues
+ * nothing (n = 0) does not advance the counter.  Collective rule: every rank
+ * creates its state from the same schedule and first_iter and makes the same
+ * calls (the schedule, not the iteration, is part of the call signature).
+ *   firecaffe_lr_state_create   first_iter >= 0; FC_ERR_INVALID_ARG for an
+ *                               invalid schedule (as firecaffe_lr_at)
+ *   firecaffe_lr_state_get_iter synchronous: waits for the device, then reads
+ *   firecaffe_lr_state_set_iter synchronous: waits for the device, then writes
+ *                               (resume from a checkpoint)
+ * The state must be used on its device (else FC_ERR_MISMATCH) and by one
+ * stream at a time. */
+typedef struct fc_lr_state fc_lr_state;
+fc_status firecaffe_lr_state_create(const fc_lr_schedule* sched, int64_t first_iter, fc_lr_state** out);
+fc_status firecaffe_lr_state_destroy(fc_lr_state* state);
+fc_status firecaffe_lr_state_get_iter(const fc_lr_state* state, int64_t* iter);
+fc_status firecaffe_lr_state_set_iter(fc_lr_state* state, int64_t iter);
+fc_status firecaffe_sgd_step_sched(float* w, const float* grad, float* mom, int64_t n,
+                                   fc_lr_state* lr, float mu, float wd, int64_t batch,
+                                   const fc_segments* segs, void* stream);
+fc_status firecaffe_tree_allreduce_sgd_sched(float* w, float* grad, float* mom, int64_t n,
+                                             fc_lr_state* lr, float mu, float wd, int64_t batch,
+                                             const fc_segments* segs, fc_world* world, void* stream);
 
 /* firecaffe_allgather_owned — every rank's firecaffe_owned_range slice of the
  * symmetric buffer `buf` is copied to every other rank, in place: afterwards all

@@ -199,9 +199,7 @@ def firecaffe_tree_allreduce_sgd_host(w, grad, mom, grad_host, w_host, lr, mu, w
           "firecaffe_tree_allreduce_sgd_host")
 
 
-def firecaffe_lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, stepsize: int = 0, steps=(),
-                    power: float = 0.5, max_iter: int = 0) -> float:
-    """Learning rate of the paper's schedules at iteration `it` (header: firecaffe_lr_at)."""
+def _schedule(policy: str, base_lr: float, gamma: float, stepsize: int, steps, power: float, max_iter: int):
     s = _lib.FcLrSchedule()
     s.policy = _lib.LR_POLICY[policy]
     s.base_lr, s.gamma, s.stepsize, s.power, s.max_iter = base_lr, gamma, int(stepsize), power, int(max_iter)
@@ -210,7 +208,65 @@ def firecaffe_lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, st
     s.nsteps = len(steps)
     for i, v in enumerate(steps):
         s.steps[i] = int(v)
+    return s
+
+
+def firecaffe_lr_at(policy: str, base_lr: float, it: int, gamma: float = 0.1, stepsize: int = 0, steps=(),
+                    power: float = 0.5, max_iter: int = 0) -> float:
+    """Learning rate of the paper's schedules at iteration `it` (header: firecaffe_lr_at)."""
+    s = _schedule(policy, base_lr, gamma, stepsize, steps, power, max_iter)
     r = load().firecaffe_lr_at(ctypes.byref(s), int(it))
     if r < 0:
         raise ValueError("firecaffe_lr_at: invalid schedule or iteration")
     return r
+
+
+class LrState:
+    """Device-resident learning-rate schedule + iteration counter (header:
+    fc_lr_state) on the current device: the *_sched calls evaluate the schedule
+    on the GPU and advance the counter, so a captured step replays with the
+    schedule moving on."""
+
+    def __init__(self, policy: str, base_lr: float, first_iter: int = 0, gamma: float = 0.1, stepsize: int = 0,
+                 steps=(), power: float = 0.5, max_iter: int = 0):
+        s = _schedule(policy, base_lr, gamma, stepsize, steps, power, max_iter)
+        h = ctypes.c_void_p()
+        check(load().firecaffe_lr_state_create(ctypes.byref(s), int(first_iter), ctypes.byref(h)),
+              "firecaffe_lr_state_create")
+        self.handle = h.value
+
+    @property
+    def iter(self) -> int:
+        v = ctypes.c_int64()
+        check(load().firecaffe_lr_state_get_iter(self.handle, ctypes.byref(v)), "firecaffe_lr_state_get_iter")
+        return v.value
+
+    @iter.setter
+    def iter(self, it: int):
+        check(load().firecaffe_lr_state_set_iter(self.handle, int(it)), "firecaffe_lr_state_set_iter")
+
+    def close(self):
+        if self.handle:
+            load().firecaffe_lr_state_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def firecaffe_sgd_step_sched(w, grad, mom, lr: LrState, mu, wd, batch, segs=None, n=None, stream=None):
+    """firecaffe_sgd_step with lr from the device-resident schedule (advanced by one)."""
+    check(load().firecaffe_sgd_step_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr.handle, mu, wd,
+                                          int(batch), segs.handle if segs else None, _stream(stream)),
+          "firecaffe_sgd_step_sched")
+
+
+def firecaffe_tree_allreduce_sgd_sched(w, grad, mom, lr: LrState, mu, wd, batch, world: "World", segs=None,
+                                       n=None, stream=None):
+    """firecaffe_tree_allreduce_sgd with lr from the device-resident schedule (advanced by one)."""
+    check(load().firecaffe_tree_allreduce_sgd_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr.handle, mu,
+                                                    wd, int(batch), segs.handle if segs else None, world.handle,
+                                                    _stream(stream)), "firecaffe_tree_allreduce_sgd_sched")

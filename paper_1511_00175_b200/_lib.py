@@ -69,6 +69,12 @@ SIGNATURES = {
     "firecaffe_tree_allreduce_sgd_bf16": (_I, [_P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
     "firecaffe_sgd_step_host": (_I, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P]),
     "firecaffe_tree_allreduce_sgd_host": (_I, [_P, _P, _P, _P, _P, _I64, _F, _F, _F, _I64, _P, _P, _P]),
+    "firecaffe_lr_state_create": (_I, [_P, _I64, _PP]),
+    "firecaffe_lr_state_destroy": (_I, [_P]),
+    "firecaffe_lr_state_get_iter": (_I, [_P, _PI64]),
+    "firecaffe_lr_state_set_iter": (_I, [_P, _I64]),
+    "firecaffe_sgd_step_sched": (_I, [_P, _P, _P, _I64, _P, _F, _F, _I64, _P, _P]),
+    "firecaffe_tree_allreduce_sgd_sched": (_I, [_P, _P, _P, _I64, _P, _F, _F, _I64, _P, _P, _P]),
 }
 
 FC_LR_MAX_STEPS = 16

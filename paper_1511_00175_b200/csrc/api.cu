@@ -25,6 +25,13 @@ struct fc_segments {
     float* d_dm;
 };
 
+struct fc_lr_state {
+    FcLrDev* d;         // device copy of the schedule + the iteration counter
+    fc_lr_schedule s;   // host copy (validation, call signature)
+    int device;
+    uint32_t hash;      // of the schedule: part of the collective call signature
+};
+
 struct fc_world {
     int rank;  // -1 for a virtual world
     int p;
@@ -361,7 +368,8 @@ fc_status firecaffe_owned_range(const fc_world* w, int rank, int64_t n, int64_t*
 }
 
 static fc_status sgd_impl(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
-                          float wd, int64_t batch, const fc_segments* segs, void* stream);
+                          float wd, int64_t batch, const fc_segments* segs, void* stream,
+                          const fc_lr_state* lrst = nullptr);
 
 fc_status firecaffe_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr,
                              float mu, float wd, int64_t batch, void* stream) {
@@ -392,8 +400,16 @@ static fc_status check_segs(const fc_segments* segs, int64_t n, FcSegs* out) {
     return FC_OK;
 }
 
+static fc_status check_lr_state(const fc_lr_state* lrst) {
+    if (!lrst) return FC_OK;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
+    return cur == lrst->device ? FC_OK : FC_ERR_MISMATCH;
+}
+
 static fc_status sgd_impl(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
-                          float wd, int64_t batch, const fc_segments* segs, void* stream) {
+                          float wd, int64_t batch, const fc_segments* segs, void* stream,
+                          const fc_lr_state* lrst) {
     if (n < 0) return FC_ERR_INVALID_ARG;
     fc_status st = check_hyper(lr, mu, wd, batch);
     if (st != FC_OK) return st;
@@ -405,8 +421,9 @@ static fc_status sgd_impl(float* w, const float* grad, float* mom, int64_t n, fl
     FcSegs sd;
     st = check_segs(segs, n, &sd);
     if (st != FC_OK) return st;
+    if ((st = check_lr_state(lrst)) != FC_OK) return st;
     cudaError_t e = launch_sgd_step(w, grad, mom, n, lr, mu, wd, inv_batch(batch), sd,
-                                    (cudaStream_t)stream);
+                                    (cudaStream_t)stream, lrst ? lrst->d : nullptr);
     return e == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 
@@ -421,7 +438,8 @@ static int64_t heap_offset(const fc_world* w, const void* p, int64_t n) {
 
 static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* mom, int64_t n,
                             float lr, float mu, float wd, int64_t batch,
-                            const fc_segments* segs, void* stream, int win_k = 0, int win_s = 1) {
+                            const fc_segments* segs, void* stream, int win_k = 0, int win_s = 1,
+                            const fc_lr_state* lrst = nullptr) {
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess) return FC_ERR_CUDA;
     if (cur != w->device) return FC_ERR_MISMATCH;
@@ -449,6 +467,12 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         fc_status st = check_segs(segs, n, &c.segs);
         if (st != FC_OK) return st;
         if (segs) seg_hash = segs->hash;
+        if ((st = check_lr_state(lrst)) != FC_OK) return st;
+        if (lrst) {
+            c.lrs = lrst->d;
+            c.lr = 0.0f;
+            seg_hash ^= lrst->hash * 0x9e3779b1u;  // the schedule replaces lr in the signature
+        }
     }
     for (int q = 0; q < w->p; ++q) c.peers.heap[q] = w->peer[q];
     c.rank = w->virt ? -1 : w->rank;
@@ -534,7 +558,7 @@ fc_status firecaffe_ps_allreduce(float* grad, int64_t n, fc_world* w, void* stre
 
 static fc_status fused_impl(float* wt, float* grad, float* mom, int64_t n, float lr, float mu,
                             float wd, int64_t batch, const fc_segments* segs, fc_world* w,
-                            void* stream) {
+                            void* stream, const fc_lr_state* lrst = nullptr) {
     if (!w || n < 0) return FC_ERR_INVALID_ARG;
     fc_status st = check_hyper(lr, mu, wd, batch);
     if (st != FC_OK) return st;
@@ -543,8 +567,9 @@ static fc_status fused_impl(float* wt, float* grad, float* mom, int64_t n, float
     const int64_t bytes = n * 4;
     if (overlap(wt, grad, bytes) || overlap(wt, mom, bytes) || overlap(grad, mom, bytes))
         return FC_ERR_INVALID_ARG;
-    if (w->p == 1) return sgd_impl(wt, grad, mom, n, lr, mu, wd, batch, segs, stream);
-    return collective(w, FC_OP_ALLREDUCE_SGD, wt, grad, mom, n, lr, mu, wd, batch, segs, stream);
+    if (w->p == 1) return sgd_impl(wt, grad, mom, n, lr, mu, wd, batch, segs, stream, lrst);
+    return collective(w, FC_OP_ALLREDUCE_SGD, wt, grad, mom, n, lr, mu, wd, batch, segs, stream, 0, 1,
+                      lrst);
 }
 
 fc_status firecaffe_tree_allreduce_sgd(float* wt, float* grad, float* mom, int64_t n, float lr,
@@ -851,34 +876,93 @@ fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
     return cudaStreamWaitEvent(user, world->hp_start, 0) == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 
-// The paper's learning-rate schedules, in double, one
-// rounding to fp32 (R21).
-float firecaffe_lr_at(const fc_lr_schedule* s, int64_t iter) {
-    if (!s || iter < 0 || !(s->base_lr > 0.0f)) return -1.0f;
-    double f;
+// The paper's learning-rate schedules: fc_lr_factor
+// (fc_internal.h), the same arithmetic the *_sched kernels evaluate on the
+// device, one rounding to fp32 (R21).
+static bool valid_schedule(const fc_lr_schedule* s) {
+    if (!s || !(s->base_lr > 0.0f) || !std::isfinite(s->base_lr)) return false;
     switch (s->policy) {
         case FC_LR_FIXED:
-            f = 1.0;
-            break;
+            return true;
         case FC_LR_STEP:
-            if (s->stepsize < 1) return -1.0f;
-            f = std::pow((double)s->gamma, (double)(iter / s->stepsize));
-            break;
-        case FC_LR_MULTISTEP: {
-            if (s->nsteps < 0 || s->nsteps > FC_LR_MAX_STEPS) return -1.0f;
-            int k = 0;
-            for (int j = 0; j < s->nsteps; ++j) k += s->steps[j] <= iter;
-            f = std::pow((double)s->gamma, (double)k);
-            break;
-        }
+            return s->stepsize >= 1 && std::isfinite(s->gamma);
+        case FC_LR_MULTISTEP:
+            return s->nsteps >= 0 && s->nsteps <= FC_LR_MAX_STEPS && std::isfinite(s->gamma);
         case FC_LR_POLY:
-            if (s->max_iter < 1 || iter > s->max_iter) return -1.0f;
-            f = std::pow(1.0 - (double)iter / (double)s->max_iter, (double)s->power);
-            break;
-        default:
-            return -1.0f;
+            return s->max_iter >= 1 && std::isfinite(s->power);
     }
-    return (float)((double)s->base_lr * f);
+    return false;
+}
+
+float firecaffe_lr_at(const fc_lr_schedule* s, int64_t iter) {
+    if (!valid_schedule(s) || iter < 0) return -1.0f;
+    if (s->policy == FC_LR_POLY && iter > s->max_iter) return -1.0f;
+    return fc_lr_value(*s, iter);
+}
+
+fc_status firecaffe_lr_state_create(const fc_lr_schedule* sched, int64_t first_iter,
+                                    fc_lr_state** out) {
+    if (!out) return FC_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!valid_schedule(sched) || first_iter < 0) return FC_ERR_INVALID_ARG;
+    fc_lr_state* t = new fc_lr_state();
+    memset(t, 0, sizeof(*t));
+    t->s = *sched;
+    if (t->s.policy != FC_LR_MULTISTEP) t->s.nsteps = 0;
+    for (int j = t->s.nsteps; j < FC_LR_MAX_STEPS; ++j) t->s.steps[j] = 0;
+    uint32_t h = 2166136261u;
+    const unsigned char* b = (const unsigned char*)&t->s;
+    for (size_t i = 0; i < sizeof(t->s); ++i) h = (h ^ b[i]) * 16777619u;
+    t->hash = h;
+    FcLrDev init;
+    memset(&init, 0, sizeof(init));
+    init.s = t->s;
+    init.iter = first_iter;
+    if (cudaGetDevice(&t->device) != cudaSuccess || cudaMalloc(&t->d, sizeof(FcLrDev)) != cudaSuccess ||
+        cudaMemcpy(t->d, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        firecaffe_lr_state_destroy(t);
+        return FC_ERR_CUDA;
+    }
+    *out = t;
+    return FC_OK;
+}
+
+fc_status firecaffe_lr_state_destroy(fc_lr_state* t) {
+    if (!t) return FC_OK;
+    if (t->d) cudaFree(t->d);
+    delete t;
+    return FC_OK;
+}
+
+fc_status firecaffe_lr_state_get_iter(const fc_lr_state* t, int64_t* iter) {
+    if (!t || !iter) return FC_ERR_INVALID_ARG;
+    if (cudaDeviceSynchronize() != cudaSuccess) return FC_ERR_CUDA;
+    return cudaMemcpy(iter, &t->d->iter, sizeof(int64_t), cudaMemcpyDeviceToHost) == cudaSuccess
+               ? FC_OK
+               : FC_ERR_CUDA;
+}
+
+fc_status firecaffe_lr_state_set_iter(fc_lr_state* t, int64_t iter) {
+    if (!t || iter < 0) return FC_ERR_INVALID_ARG;
+    if (cudaDeviceSynchronize() != cudaSuccess) return FC_ERR_CUDA;
+    return cudaMemcpy(&t->d->iter, &iter, sizeof(int64_t), cudaMemcpyHostToDevice) == cudaSuccess
+               ? FC_OK
+               : FC_ERR_CUDA;
+}
+
+fc_status firecaffe_sgd_step_sched(float* w, const float* grad, float* mom, int64_t n,
+                                   fc_lr_state* lr, float mu, float wd, int64_t batch,
+                                   const fc_segments* segs, void* stream) {
+    if (!lr) return FC_ERR_INVALID_ARG;
+    return sgd_impl(w, grad, mom, n, 1.0f, mu, wd, batch, segs, stream, lr);
+}
+
+fc_status firecaffe_tree_allreduce_sgd_sched(float* wt, float* grad, float* mom, int64_t n,
+                                             fc_lr_state* lr, float mu, float wd, int64_t batch,
+                                             const fc_segments* segs, fc_world* w, void* stream) {
+    if (!lr) return FC_ERR_INVALID_ARG;
+    return fused_impl(wt, grad, mom, n, 1.0f, mu, wd, batch, segs, w, stream, lr);
 }
 
 void firecaffe_tune_sgd_unroll(int u) { set_sgd_unroll(u); }

@@ -71,10 +71,22 @@ __device__ __forceinline__ void trace(const FcColl& c, int slot) {
 // the last CTA to finish publishes the next one (stream order makes it visible
 // to the next launch).  All ranks make the same calls, so the counters agree.
 __shared__ uint32_t s_epoch;
+// The call's learning rate: the argument, or (c.lrs, the *_sched entry points)
+// the device-resident schedule at its current iteration, evaluated once per CTA.
+__shared__ float s_lr;
 
 __device__ __forceinline__ void epoch_begin(const FcColl& c) {
-    if (threadIdx.x == 0) s_epoch = *(volatile uint32_t*)c.ctl + 1u;
+    if (threadIdx.x == 0) {
+        s_epoch = *(volatile uint32_t*)c.ctl + 1u;
+        s_lr = c.lrs ? fc_lr_value(c.lrs->s, *(volatile int64_t*)&c.lrs->iter) : c.lr;
+    }
     __syncthreads();
+}
+
+// Last CTA of a call: the schedule's next call uses the next iteration (every
+// CTA of this call read `iter` at entry, before arriving on the counter).
+__device__ __forceinline__ void advance_lr(const FcColl& c) {
+    if (c.lrs) c.lrs->iter = c.lrs->iter + 1;
 }
 
 __device__ __forceinline__ void epoch_end(const FcColl& c) {
@@ -85,6 +97,7 @@ __device__ __forceinline__ void epoch_end(const FcColl& c) {
         const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
         if (done == total) {
             c.ctl[1] = 0u;
+            advance_lr(c);
             __threadfence();
             atomicExch(c.ctl, s_epoch);
         }
@@ -190,6 +203,7 @@ static __device__ __noinline__ void exit_rank(const FcColl& c, int rank) {
         }
     }
     c.ctl[1] = 0u;
+    advance_lr(c);
     __threadfence();
     atomicExch(c.ctl, s_epoch);
 }
@@ -305,7 +319,7 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
         const int k = j * TREE_T + t;
         if (k < nf4) {
             const float4 s = add4(a[j], b[j]);
-            sgd4_any(c.segs, e0 + 4 * (int64_t)k, s, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+            sgd4_any(c.segs, e0 + 4 * (int64_t)k, s, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
             st_na(w4 + k, w[j]);
             st_na(v4 + k, v[j]);
             if (push) {
@@ -321,7 +335,7 @@ __device__ __forceinline__ void reduce_chunk(const FcColl& c, int rank, int64_t 
         float* wp = w_of(c, rank) + e;
         float* vp = mom_of(c, rank) + e;
         float ww = *wp, vv = *vp;
-        sgd1_any(c.segs, e, s, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+        sgd1_any(c.segs, e, s, ww, vv, s_lr, c.mu, c.wd, c.inv_b);
         st1(wp, ww);
         st1(vp, vv);
         if (push)

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
 #pragma unroll
                         for (int q = 0; q < P; ++q) f[q] = bf16x4_to_f32(x[j][q]);
                         const float4 S = tree_sum_regs<P, K>(f);
-                        sgd4_any(c.segs, 4 * i, S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                        sgd4_any(c.segs, 4 * i, S, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
                         st_na(v4 + i, v[j]);
 #pragma unroll
                         for (int q = 0; q < P; ++q) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
                 for (int q = 0; q < P; ++q) xs[q] = bf16_to_f32(gradh_of(c, q)[e]);
                 const float S = tree_sum_regs1<P, K>(xs);
                 float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
-                sgd1_any(c.segs, e, S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                sgd1_any(c.segs, e, S, ww, vv, s_lr, c.mu, c.wd, c.inv_b);
                 st1(mom_of(c, rank) + e, vv);
                 for (int q = 0; q < P; ++q) st1(w_of(c, q) + e, ww);
             }

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                         const int64_t i = base + j * T;
                         if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
-                            sgd4_any(c.segs, 4 * i, S, w[j], v[j], c.lr, c.mu, c.wd, c.inv_b);
+                            sgd4_any(c.segs, 4 * i, S, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
                             st_na(v4 + i, v[j]);
 #pragma unroll
                             for (int q = 0; q < P; ++q)
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                 const float S = tree_sum_regs1<P, K>(xs);
                 if (fused) {
                     float ww = w_of(c, rank)[e], vv = mom_of(c, rank)[e];
-                    sgd1_any(c.segs, e, S, ww, vv, c.lr, c.mu, c.wd, c.inv_b);
+                    sgd1_any(c.segs, e, S, ww, vv, s_lr, c.mu, c.wd, c.inv_b);
                     st1(mom_of(c, rank) + e, vv);
                     for (int q = 0; q < P; ++q)
                         if (!pull || q == rank) st1(w_of(c, q) + e, ww);

@@ -1,5 +1,6 @@
 // Internal host/device structures of libfirecaffe (not part of the C ABI).
 #pragma once
+#include <math.h>
 #include <stdint.h>
 
 #include "../../include/firecaffe.h"
@@ -42,6 +43,61 @@ struct FcSegs {
     int nseg;
 };
 
+#ifdef __CUDACC__
+#define FC_HD __host__ __device__
+#else
+#define FC_HD
+#endif
+
+// Learning-rate factor of the paper's schedules at iteration `iter` (DESIGN.md
+// R21), the same arithmetic on the host (firecaffe_lr_at) and on the device
+// (the *_sched entry points): STEP / MULTISTEP gamma^k by binary powering in
+// double (k = 1, 2: gamma, fl(gamma^2)); POLY (1 - iter/max_iter)^power in
+// double, power 0.5 (the paper's) as the correctly rounded sqrt, power
+// 1 as the base itself, others through pow; 0 at and after max_iter.  The
+// caller validates the schedule.
+FC_HD inline double fc_lr_factor(const fc_lr_schedule& s, int64_t iter) {
+    int64_t k = 0;
+    switch (s.policy) {
+        case FC_LR_STEP:
+            k = iter / s.stepsize;
+            break;
+        case FC_LR_MULTISTEP:
+            for (int j = 0; j < s.nsteps; ++j) k += s.steps[j] <= iter;
+            break;
+        case FC_LR_POLY: {
+            if (iter >= s.max_iter) return 0.0;
+            const double x = 1.0 - (double)iter / (double)s.max_iter;
+            if (s.power == 0.5f) return sqrt(x);
+            if (s.power == 1.0f) return x;
+            return pow(x, (double)s.power);
+        }
+        default:
+            return 1.0;
+    }
+    double f = 1.0, b = (double)s.gamma;
+    while (k > 0) {
+        if (k & 1) f *= b;
+        k >>= 1;
+        if (k) b *= b;
+    }
+    return f;
+}
+
+// fl32(base_lr * factor): one rounding of the double product to fp32
+FC_HD inline float fc_lr_value(const fc_lr_schedule& s, int64_t iter) {
+    return (float)((double)s.base_lr * fc_lr_factor(s, iter));
+}
+
+// Device-resident schedule state of the *_sched entry points: the schedule,
+// the iteration the next call uses, and the CTA arrival counter with which the
+// last CTA of a call advances `iter` (stream order publishes it to the next call).
+struct FcLrDev {
+    fc_lr_schedule s;
+    int64_t iter;
+    uint32_t done;
+};
+
 // Everything a collective kernel needs to find every rank's buffers.
 struct FcPeers {
     char* heap[FC_MAX_RANKS];  // each rank's heap base, as mapped in this process
@@ -62,6 +118,7 @@ struct FcColl {
     int64_t off_mom;   // >= 0: mom is symmetric in the heap; < 0: use mom_local
     float* mom_local;
     float lr, mu, wd, inv_b;
+    FcLrDev* lrs;      // non-null: lr = the schedule at lrs->iter (device), advanced once per call
     FcSegs segs;       // per-blob multipliers for the fused update
     int bcast;         // fc_bcast
     int owner_single_root;  // ownership of the single-root schedule (rank 0 owns all)

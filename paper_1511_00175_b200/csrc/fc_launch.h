@@ -14,11 +14,14 @@ struct DevInfo {
 const DevInfo& dev_info();  // current device's SM count (cached per device)
 int occupancy(const void* fn, int block);  // resident CTAs/SM, cached per (kernel, block, device)
 
+// lrs non-null (firecaffe_sgd_step_sched): lr comes from the device-resident
+// schedule at its current iteration, which the kernel advances by one.
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
-                            float wd, float inv_b, const FcSegs& segs, cudaStream_t st);
+                            float wd, float inv_b, const FcSegs& segs, cudaStream_t st,
+                            FcLrDev* lrs = nullptr);
 cudaError_t launch_sgd_step_range(float* w, const float* grad, float* mom, int64_t off, int64_t len,
                                   float lr, float mu, float wd, float inv_b, const FcSegs& segs,
-                                  cudaStream_t st);
+                                  cudaStream_t st, FcLrDev* lrs = nullptr);
 void set_sgd_unroll(int u);
 cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int64_t n, float lr,
                                  float mu, float wd, float inv_b, const FcSegs& segs,

@@ -19,7 +19,14 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                                                        const float* __restrict__ gt,
                                                        float* __restrict__ vt, int tail, float lr,
                                                        float mu, float wd, float inv_b,
-                                                       const FcSegs segs, int64_t elem0) {
+                                                       const FcSegs segs, int64_t elem0,
+                                                       FcLrDev* lrs) {
+    if (lrs) {  // firecaffe_sgd_step_sched: the schedule at its current iteration
+        __shared__ float s_lr;
+        if (threadIdx.x == 0) s_lr = fc_lr_value(lrs->s, *(volatile int64_t*)&lrs->iter);
+        __syncthreads();
+        lr = s_lr;
+    }
     const int64_t T = blockDim.x;
     const int64_t stride = (int64_t)gridDim.x * T * U;
     for (int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x; base < n4; base += stride) {
@@ -50,6 +57,17 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
         sgd1_any(segs, elem0 + 4 * n4 + t, gt[t], w, v, lr, mu, wd, inv_b);
         wt[t] = w;
         vt[t] = v;
+    }
+    if (lrs) {  // the last CTA to finish advances the iteration (all CTAs read it at entry)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&lrs->done, 1u) + 1u == gridDim.x) {
+                lrs->done = 0u;
+                lrs->iter = lrs->iter + 1;
+                __threadfence();
+            }
+        }
     }
 }
 
@@ -124,14 +142,14 @@ cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int
 static int g_sgd_unroll = 4;
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
-                            float wd, float inv_b, const FcSegs& segs, cudaStream_t st) {
-    return launch_sgd_step_range(w, grad, mom, 0, n, lr, mu, wd, inv_b, segs, st);
+                            float wd, float inv_b, const FcSegs& segs, cudaStream_t st, FcLrDev* lrs) {
+    return launch_sgd_step_range(w, grad, mom, 0, n, lr, mu, wd, inv_b, segs, st, lrs);
 }
 
 // Elements [off, off + len) (off a multiple of 4); blob lookups use absolute indices.
 cudaError_t launch_sgd_step_range(float* w0, const float* grad0, float* mom0, int64_t off,
                                   int64_t len, float lr, float mu, float wd, float inv_b,
-                                  const FcSegs& segs, cudaStream_t st) {
+                                  const FcSegs& segs, cudaStream_t st, FcLrDev* lrs) {
     float* w = w0 + off;
     const float* grad = grad0 + off;
     float* mom = mom0 + off;
@@ -149,7 +167,7 @@ cudaError_t launch_sgd_step_range(float* w0, const float* grad0, float* mom0, in
         if (grid < 1) grid = 1;
         kern<<<(unsigned)grid, T, 0, st>>>((float4*)w, (const float4*)grad, (float4*)mom, n4,
                                            w + n4 * 4, grad + n4 * 4, mom + n4 * 4, tail, lr, mu,
-                                           wd, inv_b, segs, off);
+                                           wd, inv_b, segs, off, lrs);
         return cudaGetLastError();
     };
     switch (g_sgd_unroll) {

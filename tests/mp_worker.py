@@ -101,6 +101,26 @@ def main():
             fails.append(f"segments w n={n}")
         if not np.array_equal(bits(mom[:n]), vs_ref.view(np.uint32)):
             fails.append(f"allgathered mom n={n}")
+        # on-device lr schedule: 3 steps, lr drops after steps 1 and 2
+        W.config("flat", "direct", 2)
+        lrs = fc.LrState("multistep", 0.04, first_iter=0, gamma=0.1, steps=(1, 2))
+        w[:n].copy_(w0)
+        mom[:n].copy_(v0)
+        wk, vk = w0.numpy(), v0.numpy()
+        for it in range(3):
+            grad[:n].copy_(g_all[rank])
+            fc.firecaffe_tree_allreduce_sgd_sched(w, grad, mom, lrs, HP["mu"], HP["wd"], HP["batch"], W, n=n)
+            wk, vk = oracle.sgd(wk, vk, s_ref, oracle.lr_at("multistep", 0.04, it, gamma=0.1, steps=(1, 2)),
+                                HP["mu"], HP["wd"], HP["batch"])
+        torch.cuda.synchronize()
+        if not np.array_equal(bits(w[:n]), wk.view(np.uint32)):
+            fails.append(f"sched w n={n}")
+        b, e = W.owned_range(rank, n)
+        if not np.array_equal(bits(mom[b:e]), vk[b:e].view(np.uint32)):
+            fails.append(f"sched mom n={n}")
+        if lrs.iter != 3:
+            fails.append(f"sched iter {lrs.iter} != 3")
+        lrs.close()
         # host-buffer entry point (pinned grad in, pinned weights out)
         W.config("flat", "direct", 2)
         g_host = g_all[rank].clone().pin_memory()

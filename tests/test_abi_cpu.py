@@ -4,6 +4,7 @@ its host-only helpers behave as documented."""
 import os
 import re
 
+import numpy as np
 import pytest
 
 import paper_1511_00175_b200 as fc
@@ -103,6 +104,50 @@ def test_lr_schedules_match_oracle(policy, kw):
             if policy == "poly" and it > kw["max_iter"]:
                 continue
             assert fc.firecaffe_lr_at(policy, base, it, **kw) == oracle.lr_at(policy, base, it, **kw)
+
+
+@pytest.mark.parametrize("policy,base,kw,iters", [
+    ("multistep", 0.01, dict(gamma=0.1, steps=(100_000, 200_000)), range(0, 300_001, 7)),   # NiN
+    ("poly", 0.08, dict(power=0.5, max_iter=450_000), range(0, 450_001, 3)),                # GoogLeNet
+    ("poly", 0.04, dict(power=0.5, max_iter=9_973), range(0, 9_974)),
+    ("step", 0.04, dict(gamma=0.5, stepsize=10), range(0, 2_000)),
+])
+def test_lr_schedules_dense_bitexact(policy, base, kw, iters):
+    """The library's schedule arithmetic (fc_lr_factor: binary powering, sqrt for
+    power 0.5; the same code the *_sched kernels run on the device) gives the
+    oracle's lr (std::pow) bit for bit at every sampled iteration of the paper's
+    schedules."""
+    import oracle
+
+    bad = [it for it in iters
+           if np.float32(fc.firecaffe_lr_at(policy, base, it, **kw)) != np.float32(oracle.lr_at(policy, base, it, **kw))]
+    assert not bad, f"{len(bad)} iterations differ, first {bad[:5]}"
+
+
+def test_lr_schedules_random_within_one_ulp():
+    """Schedules outside the paper's (gamma^k with k >= 3, arbitrary powers): the
+    binary powering / pow of the library may differ from the oracle's std::pow
+    in the last bit of the double; after the fp32 rounding they agree to 1 ulp
+    (and almost always exactly)."""
+    import oracle
+
+    rng = np.random.default_rng(151100175)
+    exact = total = 0
+    for _ in range(300):
+        base = float(np.float32(10 ** rng.uniform(-4, -0.5)))
+        if rng.random() < 0.5:
+            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 0.99))), stepsize=int(rng.integers(1, 50)))
+            policy, its = "step", rng.integers(0, 2_000, 20)
+        else:
+            kw = dict(power=float(np.float32(rng.uniform(0.1, 3.0))), max_iter=int(rng.integers(10, 100_000)))
+            policy, its = "poly", rng.integers(0, kw["max_iter"] + 1, 20)
+        for it in its:
+            a = np.float32(fc.firecaffe_lr_at(policy, base, int(it), **kw))
+            b = np.float32(oracle.lr_at(policy, base, int(it), **kw))
+            total += 1
+            exact += a == b
+            assert abs(int(a.view(np.int32)) - int(b.view(np.int32))) <= 1, (policy, base, kw, it, a, b)
+    assert exact >= 0.99 * total
 
 
 def test_lr_schedule_errors():

@@ -488,6 +488,149 @@ def test_cuda_graph_capture_and_replay(sched, bcast):
         W.close()
 
 
+# ------------------------------------------ on-device lr schedules (f2) --
+LR_CASES = [
+    ("multistep", 0.04, dict(gamma=0.1, steps=(2, 4))),  # NiN's "÷10 twice", compressed
+    ("poly", 0.08, dict(power=0.5, max_iter=5)),          # GoogLeNet's poly 0.5, reaches 0
+    ("step", 0.01, dict(gamma=0.5, stepsize=2)),
+    ("poly", 0.02, dict(power=2.0, max_iter=9)),
+]
+
+
+def _lr_ref(policy, base, it, kw):
+    """The oracle's lr; the device gives 0 at and after a poly max_iter (header)."""
+    if policy == "poly" and it >= kw["max_iter"]:
+        return 0.0
+    return oracle.lr_at(policy, base, it, **kw)
+
+
+@pytest.mark.parametrize("policy,base,kw", LR_CASES)
+@pytest.mark.parametrize("n,first", [(7, 0), (100_003, 0), (4097, 3)])
+def test_sgd_step_sched_bitexact(policy, base, kw, n, first):
+    """firecaffe_sgd_step_sched: the kernel evaluates the schedule at the device
+    counter and advances it; K steps == K oracle steps at the oracle's lr."""
+    K = 7
+    g = fc_inputs.grad(n, 0, seed=n + 11)
+    w0, v0 = fc_inputs.weights(n, seed=n + 12), fc_inputs.momentum(n, seed=n + 13)
+    gd, wdv, vd = g.cuda(), w0.cuda(), v0.cuda()
+    st = fc.LrState(policy, base, first_iter=first, **kw)
+    try:
+        w_ref, v_ref = w0.numpy(), v0.numpy()
+        for it in range(first, first + K):
+            fc.firecaffe_sgd_step_sched(wdv, gd, vd, st, mu=0.9, wd=5e-4, batch=1024)
+            w_ref, v_ref = oracle.sgd(w_ref, v_ref, g.numpy(), _lr_ref(policy, base, it, kw), 0.9, 5e-4, 1024)
+            torch.cuda.synchronize()
+            assert_bitexact(wdv, w_ref, f"w it {it}")
+            assert_bitexact(vd, v_ref, f"mom it {it}")
+        assert st.iter == first + K
+        st.iter = first  # rewind (resume from a checkpoint)
+        assert st.iter == first
+    finally:
+        st.close()
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "tree"), ("single_root", "direct"),
+                                         ("flat", "pull")])
+@pytest.mark.parametrize("policy,base,kw", LR_CASES[:2])
+def test_virtual_fused_sched_bitexact(p, sched, bcast, policy, base, kw):
+    """firecaffe_tree_allreduce_sgd_sched on a virtual world: one counter for the
+    whole world, advanced once per call; every rank's w and owned mom == the
+    oracle's after each of K steps."""
+    if not _sched_ok(p, sched):
+        pytest.skip("forest needs a power-of-two world")
+    n, K = 3 * 4096 + 7, 6
+    W = _world(p, n)
+    st = fc.LrState(policy, base, **kw)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=4400 + p)
+        w0, v0 = fc_inputs.weights(n, seed=44), fc_inputs.momentum(n, seed=45)
+        _fill(ws, [w0] * p)
+        _fill(moms, [v0] * p)
+        S = oracle.tree_sum(g.numpy(), 2)
+        w_ref, v_ref = w0.numpy(), v0.numpy()
+        for it in range(K):
+            _fill(grads, g)  # the fused call leaves partial sums in grad
+            fc.firecaffe_tree_allreduce_sgd_sched(ws[0], grads[0], moms[0], st, 0.9, 5e-4, 1024, W, n=n)
+            w_ref, v_ref = oracle.sgd(w_ref, v_ref, S, _lr_ref(policy, base, it, kw), 0.9, 5e-4, 1024)
+        assert W.poll() == 0
+        assert st.iter == K
+        for r in range(p):
+            assert_bitexact(ws[r], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            assert_bitexact(moms[r][b:e], v_ref[b:e], f"mom rank {r}")
+    finally:
+        st.close()
+        W.close()
+
+
+def test_cuda_graph_replays_the_schedule():
+    """A captured sched step replays with the schedule moving on (no host
+    involvement): 5 replays == 5 eager calls, bit for bit, and the lr changed
+    in between (the counter reached 5)."""
+    p, n, K = 4, 2 * 4096 + 3, 5
+    kw = dict(gamma=0.1, steps=(1, 3))
+    W = _world(p, n)
+    try:
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        g = fc_inputs.grads(n, p, seed=909)
+        w0, v0 = fc_inputs.weights(n, seed=910), fc_inputs.momentum(n, seed=911)
+
+        def reset():
+            _fill(grads, g)
+            _fill(ws, [w0] * p)
+            _fill(moms, [v0] * p)
+
+        eager = fc.LrState("multistep", 0.04, **kw)
+        reset()
+        for _ in range(K):
+            fc.firecaffe_tree_allreduce_sgd_sched(ws[0], grads[0], moms[0], eager, 0.9, 5e-4, 1024, W)
+            _fill(grads, g)
+        eager_w = [x.clone() for x in ws]
+        assert eager.iter == K
+        st = fc.LrState("multistep", 0.04, **kw)
+        reset()
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                fc.firecaffe_tree_allreduce_sgd_sched(ws[0], grads[0], moms[0], st, 0.9, 5e-4, 1024, W)
+        torch.cuda.current_stream().wait_stream(s)
+        reset()
+        for _ in range(K):
+            graph.replay()
+            torch.cuda.synchronize()
+            _fill(grads, g)
+        assert W.poll() == 0
+        assert st.iter == K
+        for r in range(p):
+            assert torch.equal(ws[r], eager_w[r]), f"w rank {r}"
+        # and the schedule really moved: a fixed-lr replay differs
+        S = oracle.tree_sum(g.numpy(), 2)
+        wf, vf = w0.numpy(), v0.numpy()
+        for _ in range(K):
+            wf, vf = oracle.sgd(wf, vf, S, 0.04, 0.9, 5e-4, 1024)
+        assert not np.array_equal(_bits(ws[0]), _bits(wf))
+        eager.close()
+        st.close()
+    finally:
+        W.close()
+
+
+def test_sched_rejects_bad_args():
+    with pytest.raises(Exception):
+        fc.LrState("poly", 0.01, max_iter=0)
+    with pytest.raises(Exception):
+        fc.LrState("step", 0.01, stepsize=0)
+    with pytest.raises(Exception):
+        fc.LrState("fixed", -1.0)
+    with pytest.raises(Exception):
+        fc.LrState("fixed", 0.01, first_iter=-1)
+
+
 @pytest.mark.parametrize("p", [2, 3, 4, 8])
 @pytest.mark.parametrize("sched", ["flat", "single_root"])
 def test_allgather_owned_momentum_checkpoint(p, sched):
