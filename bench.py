@@ -491,7 +491,8 @@ def main():
         if roof["traffic"] is None:
             roof["traffic_note"] = ("ncu cannot replay a cross-GPU kernel (the peers' flags never arrive); the same "
                                     "kernel in a virtual world reads exactly the algorithmic bytes from DRAM "
-                                    "(profiles/r01_ncu_flat_virtual_p4_nin.json)")
+                                    "(profiles/r01_ncu_flat_virtual_p4_nin.json); NVLink byte counters are not "
+                                    "readable on these boxes (profiles/r01_nvlink_counters_probe.txt)")
 
     # ---- baselines on the same buffers (context: PS, paper's single-root tree, NCCL, torch)
     baselines = {}
