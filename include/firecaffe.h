@@ -365,7 +365,10 @@ fc_status firecaffe_world_set_trace(fc_world* world, uint64_t* buf, int64_t capa
 int firecaffe_world_last_grid(const fc_world* world);
 
 /* Tuning knob for firecaffe_sgd_step: float4s in flight per thread per operand
- * (1, 2, 4 or 8; default 4).  Process-wide; value-neutral. */
+ * (1, 2, 4 or 8); -1, -2, -4: the same with the next iteration's loads issued
+ * before the current math (register double buffering); 0 (default): automatic
+ * (-2 below 32 M params, -1 above, the measured best on B200).  Process-wide;
+ * value-neutral. */
 void firecaffe_tune_sgd_unroll(int unroll);
 
 /* Library build identifier ("firecaffe-b200 <version> sm_100a"). */

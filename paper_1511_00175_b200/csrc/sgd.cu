@@ -11,7 +11,10 @@
 
 namespace fc {
 
-template <int U>
+// DB = true: the next grid-stride iteration's loads are issued before the
+// current iteration's math and stores (register double buffering), so a
+// thread always has loads in flight.
+template <int U, bool DB>
 __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                                                        const float4* __restrict__ g4,
                                                        float4* __restrict__ v4, int64_t n4,
@@ -29,8 +32,7 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
     }
     const int64_t T = blockDim.x;
     const int64_t stride = (int64_t)gridDim.x * T * U;
-    for (int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x; base < n4; base += stride) {
-        float4 g[U], w[U], v[U];
+    auto load = [&](int64_t base, float4* g, float4* w, float4* v) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int64_t i = base + j * T;
@@ -40,6 +42,8 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                 v[j] = ld_rw(v4 + i);
             }
         }
+    };
+    auto update = [&](int64_t base, float4* g, float4* w, float4* v) {
 #pragma unroll
         for (int j = 0; j < U; ++j) {
             const int64_t i = base + j * T;
@@ -48,6 +52,29 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                 st_na(w4 + i, w[j]);
                 st_na(v4 + i, v[j]);
             }
+        }
+    };
+    int64_t base = (int64_t)blockIdx.x * T * U + threadIdx.x;
+    if constexpr (DB) {
+        float4 g[U], w[U], v[U];
+        load(base, g, w, v);
+        while (base < n4) {
+            float4 g2[U], w2[U], v2[U];
+            load(base + stride, g2, w2, v2);
+            update(base, g, w, v);
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                g[j] = g2[j];
+                w[j] = w2[j];
+                v[j] = v2[j];
+            }
+            base += stride;
+        }
+    } else {
+        for (; base < n4; base += stride) {
+            float4 g[U], w[U], v[U];
+            load(base, g, w, v);
+            update(base, g, w, v);
         }
     }
     // the n % 4 trailing elements
@@ -139,7 +166,11 @@ cudaError_t launch_sgd_step_bf16(float* w, const uint16_t* grad, float* mom, int
     return cudaGetLastError();
 }
 
-static int g_sgd_unroll = 4;
+// 0 = automatic: register double-buffered, U = 2 below 32 M params and U = 1
+// above (measured on B200, scripts/gpu_sgd_db.sh, profiles/r01_sgd_db.jsonl:
+// NiN 22.6 vs 22.9 us, AlexNet 186 vs 192 us, VGG-19 445 vs 463 us against
+// the single-buffered U = 4 kernel); tune_sgd_unroll(u) forces one shape.
+static int g_sgd_unroll = 0;
 
 cudaError_t launch_sgd_step(float* w, const float* grad, float* mom, int64_t n, float lr, float mu,
                             float wd, float inv_b, const FcSegs& segs, cudaStream_t st, FcLrDev* lrs) {
@@ -170,11 +201,15 @@ cudaError_t launch_sgd_step_range(float* w0, const float* grad0, float* mom0, in
                                            wd, inv_b, segs, off, lrs);
         return cudaGetLastError();
     };
-    switch (g_sgd_unroll) {
-        case 1: return run(sgd_step_kernel<1>, 1);
-        case 2: return run(sgd_step_kernel<2>, 2);
-        case 8: return run(sgd_step_kernel<8>, 8);
-        default: return run(sgd_step_kernel<4>, 4);
+    const int u = g_sgd_unroll != 0 ? g_sgd_unroll : (n < ((int64_t)32 << 20) ? -2 : -1);
+    switch (u) {  // < 0: double-buffered with |u|
+        case 1: return run(sgd_step_kernel<1, false>, 1);
+        case 2: return run(sgd_step_kernel<2, false>, 2);
+        case 8: return run(sgd_step_kernel<8, false>, 8);
+        case -1: return run(sgd_step_kernel<1, true>, 1);
+        case -2: return run(sgd_step_kernel<2, true>, 2);
+        case -4: return run(sgd_step_kernel<4, true>, 4);
+        default: return run(sgd_step_kernel<4, false>, 4);
     }
 }
 

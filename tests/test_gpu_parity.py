@@ -63,7 +63,7 @@ def test_sgd_step_bitexact(n, zero_mom):
     assert_bitexact(vd, v_ref, "v")
 
 
-@pytest.mark.parametrize("unroll", [1, 2, 4, 8])
+@pytest.mark.parametrize("unroll", [1, 2, 4, 8, -1, -2, -4, 0])
 @pytest.mark.parametrize("dist", ["mixed", "subnormal", "cancel"])
 def test_sgd_step_distributions_and_unroll(unroll, dist):
     n = 70_001
@@ -79,7 +79,7 @@ def test_sgd_step_distributions_and_unroll(unroll, dist):
             assert_bitexact(wd_, w_ref, f"w {hp}")
             assert_bitexact(vd, v_ref, f"v {hp}")
     finally:
-        fc.firecaffe_tune_sgd_unroll(4)
+        fc.firecaffe_tune_sgd_unroll(0)
 
 
 def test_sgd_step_spec_examples():
