@@ -1,4 +1,5 @@
 # usage: bash scripts/gpu_flat_db.sh — FLAT single- vs register double-buffered (FC_FLAT_DB), p = 2, 4; parity first
+# (FC_FLAT_DB selected a register double-buffered FLAT build that was measured, not adopted and removed; kept as the record of the experiment)
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "every_kernel_build and FC_FLAT_DB" > gpurun_out/flatdb_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/flatdb_pytest.log
 for p in 2 4; do
