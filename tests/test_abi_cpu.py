@@ -208,3 +208,28 @@ def test_host_argument_errors_without_gpu():
     assert L.firecaffe_tree_allreduce(None, 4, None, None) == _lib.FC_ERR_INVALID_ARG
     assert L.firecaffe_world_config(None, 2, 0, 0) == _lib.FC_ERR_INVALID_ARG
     assert L.firecaffe_world_create_virtual(9, 0, None, 1 << 20, 0, None) == _lib.FC_ERR_INVALID_ARG
+
+
+def test_lr_state_argument_errors_without_gpu():
+    """The on-device schedule's host checks run before any CUDA call."""
+    import ctypes
+
+    L = _lib.load()
+    out = ctypes.c_void_p()
+    bad = [fc._schedule("poly", 0.01, 0.1, 0, (), 0.5, 0),      # max_iter < 1
+           fc._schedule("step", 0.01, 0.1, 0, (), 0.5, 0),      # stepsize < 1
+           fc._schedule("fixed", -0.01, 0.1, 0, (), 0.5, 0),    # base_lr <= 0
+           fc._schedule("step", 0.01, float("nan"), 5, (), 0.5, 0)]
+    for s in bad:
+        assert L.firecaffe_lr_state_create(ctypes.byref(s), 0, ctypes.byref(out)) == _lib.FC_ERR_INVALID_ARG
+        assert not out.value
+    good = fc._schedule("fixed", 0.01, 0.1, 0, (), 0.5, 0)
+    assert L.firecaffe_lr_state_create(ctypes.byref(good), -1, ctypes.byref(out)) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_lr_state_create(ctypes.byref(good), 0, None) == _lib.FC_ERR_INVALID_ARG
+    # a sched call without a state is refused; so are the plain calls' argument errors
+    assert L.firecaffe_sgd_step_sched(None, None, None, 8, None, 0.9, 0.0, 1, None, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_tree_allreduce_sgd_sched(None, None, None, 8, None, 0.9, 0.0, 1, None, None,
+                                                None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_lr_state_get_iter(None, None) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_lr_state_set_iter(None, 3) == _lib.FC_ERR_INVALID_ARG
+    assert L.firecaffe_lr_state_destroy(None) == _lib.FC_OK
