@@ -143,6 +143,17 @@ static int exit_mode() {
     return m;
 }
 
+// FLAT work mapping (coll_flat.cuh): balanced slab rows by default;
+// FC_FLAT_MAP=stride selects the plain grid stride (A/B experiments).  Value-neutral.
+static int flat_map_stride() {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("FC_FLAT_MAP");
+        m = (e && strcmp(e, "stride") == 0) ? 1 : 0;
+    }
+    return m;
+}
+
 extern "C" {
 
 const char* firecaffe_version(void) { return FC_VERSION_STR; }
@@ -512,6 +523,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.rank_exit = exit_mode();
     c.win_k = win_k;
     c.win_s = win_s;
+    c.map_stride = flat_map_stride();
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;
@@ -525,6 +537,8 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     if (grid < 1) return FC_ERR_UNSUPPORTED;
     if (w->max_ctas > 0 && grid > w->max_ctas) grid = w->max_ctas;
     w->last_grid = grid;
+    // the grid is part of the call: the barriers pair CTAs by index across ranks
+    c.sig = (c.sig ^ (uint32_t)grid) * 16777619u;
     const int64_t need = (int64_t)grid * (w->virt ? w->p : 1) * FC_TRACE_SLOTS;
     c.trace = (w->trace && w->trace_cap >= need) ? w->trace : nullptr;
     cudaError_t e = launch_collective(c, sched, w->arity, w->virt != 0, grid, (cudaStream_t)stream);

@@ -91,16 +91,34 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
             int64_t i0 = e0 / 4, ce = i1;
             if (c.win_s > 1) window_range(e0 / 4, i1, c.win_k, c.win_s, &i0, &ce);
             const bool tail_here = c.win_s <= 1 || c.win_k == c.win_s - 1;
-            // grid-stride: all CTAs sweep the slice in lockstep, so at any moment the
+            // Work mapping.  A "slab" is G*T consecutive float4s (one per thread of the
+            // grid, coalesced); the slice is nslab slabs.  Default (balanced): rows of
+            // <= U slabs, the slabs spread evenly over ceil(nslab / U) rows, so every
+            // CTA does the same work in every row and all CTAs finish together.
+            // c.map_stride (FC_FLAT_MAP=stride): the plain grid stride, where the last
+            // partial row of G*T*U belongs to the first CTAs and the others idle.
+            // Either way all CTAs sweep the slice in lockstep, so at any moment the
             // GPU's remote reads fall in one few-MB window of each peer's heap (a
-            // contiguous range per CTA measured ~10% slower: 444 scattered streams)
-            const int64_t stride = (int64_t)gridDim.x * T * U;
-            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < ce;
-                 base += stride) {
+            // contiguous range per CTA measured ~10% slower: 444 scattered streams).
+            const int64_t GT = (int64_t)gridDim.x * T;
+            const int64_t M = ce - i0;
+            const int64_t nslab = (M + GT - 1) / GT;
+            const int64_t rows = c.map_stride ? (M + GT * U - 1) / (GT * U) : (nslab + U - 1) / U;
+            const int64_t me = c.map_stride ? (int64_t)blockIdx.x * T * U + threadIdx.x
+                                            : (int64_t)blockIdx.x * T + threadIdx.x;
+            const int64_t step = c.map_stride ? T : GT;
+            int64_t s0 = 0;
+            for (int64_t r = 0; r < rows; ++r) {
+                // element j of this thread in row r: rb + j * step, for j < nv (and < ce)
+                const int64_t s1 = c.map_stride ? 0 : nslab * (r + 1) / rows;
+                const int64_t rb = c.map_stride ? i0 + r * GT * U + me : i0 + s0 * GT + me;
+                const int nv = c.map_stride ? U : (int)(s1 - s0);
+                s0 = s1;
+#define FC_IX(j) ((j) < nv ? rb + (int64_t)(j) * step : ce)
                 float4 x[U][P];
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    const int64_t i = base + j * T;
+                    const int64_t i = FC_IX(j);
                     if (i < ce) {
 #pragma unroll
                         for (int q = 0; q < P; ++q)
@@ -113,7 +131,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                     float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
-                        const int64_t i = base + j * T;
+                        const int64_t i = FC_IX(j);
                         if (i < ce) {
                             w[j] = ld_rw(w4 + i);
                             v[j] = ld_rw(v4 + i);
@@ -121,7 +139,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                     }
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
-                        const int64_t i = base + j * T;
+                        const int64_t i = FC_IX(j);
                         if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
                             sgd4_any(c.segs, 4 * i, S, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
@@ -134,7 +152,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                 } else {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
-                        const int64_t i = base + j * T;
+                        const int64_t i = FC_IX(j);
                         if (i < ce) {
                             const float4 S = tree_sum_regs<P, K>(x[j]);
 #pragma unroll
@@ -143,6 +161,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
                         }
                     }
                 }
+#undef FC_IX
             }
             // trailing n % 4 elements of the last slice
             const int rem = (int)(e1 - 4 * i1);

@@ -126,6 +126,7 @@ struct FcColl {
     uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]
     int rank_exit;     // 1: rank-level exit (one sys fence per GPU), 0: per-CTA exit barrier
     int win_k, win_s;  // FLAT push only: process window win_k of win_s of the owned slice (win_s <= 1: all)
+    int map_stride;    // FLAT: 1 = plain grid-stride work mapping, 0 = balanced slab rows (default)
 };
 
 #define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit

@@ -248,6 +248,21 @@ def main():
         fails.append(f"offset mismatch: expected FC_ERR_MISMATCH, got {st3}")
     if not bool((g3 == float(rank + 1)).all().item()):
         fails.append("offset-mismatched call modified data")
+    # ranks launch different grids (a different CTA cap): the barriers pair CTAs by
+    # index, so this must fail the same way instead of waiting for CTAs that never come
+    W4 = fc.World.create(heap_bytes_for(4 * 4096 + 4096), timeout_s=5.0)
+    g4 = W4.alloc(4 * 4096)
+    g4.fill_(float(rank + 1))
+    W4.set_max_ctas(4 if rank == 0 else 8)
+    torch.cuda.synchronize()
+    dist.barrier()
+    fc.firecaffe_tree_allreduce(g4, W4)
+    st4 = W4.poll()
+    if st4 != 3:
+        fails.append(f"grid mismatch: expected FC_ERR_MISMATCH, got {st4}")
+    if not bool((g4 == float(rank + 1)).all().item()):
+        fails.append("grid-mismatched call modified data")
+    W4.close()
     W3.close()
     dist.barrier()
     nf = torch.tensor([len(fails)], device=dev)
