@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--size", type=int, default=7_600_000)
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--sleep", type=int, default=400_000, help="GPU cycles of delay before the pre-stamp")
+    ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush (warm L2: code, flags, data)")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -68,8 +69,9 @@ def main():
             st[2] = (1 << 62)
             st[3] = 0
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            fl_a.zero_()
-            fl_b.sum()
+            if not args.no_flush:
+                fl_a.zero_()
+                fl_b.sum()
             dist.all_reduce(tiny)
             # a long GPU-side delay: the host has enqueued everything below before the
             # GPU reaches the pre-stamp, so no host latency enters the measurement
