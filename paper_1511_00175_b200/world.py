@@ -105,13 +105,18 @@ class World:
         heap = ctypes.c_void_p()
         check(L.firecaffe_heap_alloc(self.heap_bytes, ctypes.byref(heap)), "firecaffe_heap_alloc")
         self.heap = heap.value
-        hbuf = (ctypes.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
-        check(L.firecaffe_heap_export(self.heap, hbuf), "firecaffe_heap_export")
-        handles = exchange_handles(bytes(hbuf), group, self.heap_bytes)
-        allh = (ctypes.c_uint8 * (_lib.FC_IPC_HANDLE_BYTES * self.p)).from_buffer_copy(b"".join(handles))
-        w = ctypes.c_void_p()
-        check(L.firecaffe_world_create(self.rank, self.p, self.device, self.heap, allh, self.heap_bytes,
-                                       int(timeout_s * 1e9), ctypes.byref(w)), "firecaffe_world_create")
+        try:
+            hbuf = (ctypes.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
+            check(L.firecaffe_heap_export(self.heap, hbuf), "firecaffe_heap_export")
+            handles = exchange_handles(bytes(hbuf), group, self.heap_bytes)
+            allh = (ctypes.c_uint8 * (_lib.FC_IPC_HANDLE_BYTES * self.p)).from_buffer_copy(b"".join(handles))
+            w = ctypes.c_void_p()
+            check(L.firecaffe_world_create(self.rank, self.p, self.device, self.heap, allh, self.heap_bytes,
+                                           int(timeout_s * 1e9), ctypes.byref(w)), "firecaffe_world_create")
+        except BaseException:
+            L.firecaffe_heap_free(self.heap)  # no leaked heap on a failed bootstrap
+            self.heap = None
+            raise
         self.handle = w.value
         self.layout = SymmetricLayout(self.heap_bytes, L.firecaffe_heap_reserved_bytes(self.heap_bytes))
         dist.barrier(group)  # every peer has mapped every heap before any collective runs
@@ -133,9 +138,12 @@ class World:
         check(L.firecaffe_heap_alloc(self.heap_bytes * self.p, ctypes.byref(heap)), "firecaffe_heap_alloc")
         self.heap = heap.value
         w = ctypes.c_void_p()
-        check(L.firecaffe_world_create_virtual(self.p, self.device, self.heap, self.heap_bytes,
-                                               int(timeout_s * 1e9), ctypes.byref(w)),
-              "firecaffe_world_create_virtual")
+        st = L.firecaffe_world_create_virtual(self.p, self.device, self.heap, self.heap_bytes,
+                                              int(timeout_s * 1e9), ctypes.byref(w))
+        if st != _lib.FC_OK:
+            L.firecaffe_heap_free(self.heap)
+            self.heap = None
+            check(st, "firecaffe_world_create_virtual")
         self.handle = w.value
         self.layout = SymmetricLayout(self.heap_bytes, L.firecaffe_heap_reserved_bytes(self.heap_bytes))
         return self

@@ -620,6 +620,42 @@ def test_cuda_graph_replays_the_schedule():
         W.close()
 
 
+def test_sgd_step_sched_graph_replay():
+    """1-GPU sched step captured once, replayed K times == K eager calls, and the
+    device counter moved K times (the lr dropped during the replays)."""
+    n, K = 4096 * 3 + 5, 5
+    kw = dict(gamma=0.1, steps=(1, 3))
+    g = fc_inputs.grad(n, 0, seed=71).cuda()
+    w0, v0 = fc_inputs.weights(n, seed=72).cuda(), fc_inputs.momentum(n, seed=73).cuda()
+    eager = fc.LrState("multistep", 0.04, **kw)
+    we, ve = w0.clone(), v0.clone()
+    for _ in range(K):
+        fc.firecaffe_sgd_step_sched(we, g, ve, eager, 0.9, 5e-4, 1024)
+    st = fc.LrState("multistep", 0.04, **kw)
+    wg, vg = w0.clone(), v0.clone()
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            fc.firecaffe_sgd_step_sched(wg, g, vg, st, 0.9, 5e-4, 1024)
+    torch.cuda.current_stream().wait_stream(s)
+    wg.copy_(w0)
+    vg.copy_(v0)
+    for _ in range(K):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert st.iter == K and eager.iter == K
+    assert torch.equal(wg, we) and torch.equal(vg, ve)
+    w_ref, v_ref = w0.cpu().numpy(), v0.cpu().numpy()
+    for it in range(K):
+        w_ref, v_ref = oracle.sgd(w_ref, v_ref, g.cpu().numpy(), oracle.lr_at("multistep", 0.04, it, **kw),
+                                  0.9, 5e-4, 1024)
+    assert_bitexact(wg, w_ref, "graph-replayed w")
+    eager.close()
+    st.close()
+
+
 def test_sched_rejects_bad_args():
     with pytest.raises(Exception):
         fc.LrState("poly", 0.01, max_iter=0)
