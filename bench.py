@@ -309,7 +309,10 @@ def run_reference(args):
         "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3 * n / m, 3), "ms_per_step_note": "extrapolated to the full n from the sample",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "n_params": n, "ranks": N, "batch": hp["batch"]},
+        # the same workload keys as the GPU arm's config (no device-only keys)
+        "config": {"workload": args.config, "n_params": n, "grad_bytes": 4 * n, "ranks": N,
+                   "batch": hp["batch"], "lr": hp["lr"], "mu": hp["mu"], "wd": hp["wd"],
+                   "parallelism": f"dp{N}"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
