@@ -80,8 +80,10 @@ typedef enum {
 typedef enum {
     FC_BCAST_TREE = 0,        /* mirror of the reduce levels (recursive doubling for the forest) */
     FC_BCAST_DIRECT = 1,      /* each owner pushes its slice to every peer in one level */
-    FC_BCAST_PULL = 2         /* FC_SCHED_FLAT only: owners publish their slice, every rank pulls
-                                 the others (no remote stores, no barrier after the data) */
+    FC_BCAST_PULL = 2         /* FC_SCHED_FLAT only: owners publish their slice behind a per-CTA
+                                 barrier, every rank pulls the others (no remote stores); the
+                                 rank-level exit then keeps each published slice stable until
+                                 every peer has pulled it */
 } fc_bcast;
 
 typedef struct fc_world fc_world; /* opaque; one per process (or one per virtual world) */
@@ -148,9 +150,11 @@ fc_status firecaffe_world_get_config(const fc_world* world, int* arity, fc_sched
                                      fc_bcast* bcast);
 
 /* Cap the CTAs per rank of the collective kernels (0 = automatic: one wave
- * over all SMs).  A small cap (e.g. 16) lets a collective overlap other work
- * on the GPU (bucketed overlap with the backward pass) without taking every
- * SM; every rank must use the same cap.  Value-neutral. */
+ * over all SMs; at most 1022).  A small cap (e.g. 16) lets a collective
+ * overlap other work on the GPU (bucketed overlap with the backward pass)
+ * without taking every SM; every rank must use the same cap (a rank that
+ * launches a different grid makes the call fail with FC_ERR_MISMATCH).
+ * Value-neutral. */
 fc_status firecaffe_world_set_max_ctas(fc_world* world, int max_ctas);
 
 /* Synchronise the device and return the sticky device status (FC_OK, or

@@ -991,7 +991,7 @@ fc_status firecaffe_world_set_trace(fc_world* w, uint64_t* buf, int64_t capacity
 int firecaffe_world_last_grid(const fc_world* w) { return w ? w->last_grid : 0; }
 
 fc_status firecaffe_world_set_max_ctas(fc_world* w, int max_ctas) {
-    if (!w || max_ctas < 0 || max_ctas > FC_MAX_CTAS) return FC_ERR_INVALID_ARG;
+    if (!w || max_ctas < 0 || max_ctas >= FC_EXIT_CTA_SLOT) return FC_ERR_INVALID_ARG;
     w->max_ctas = max_ctas;
     return FC_OK;
 }

@@ -169,7 +169,10 @@ static __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
 // stamp -> the peer's acquire.sys of the stamp.  The other CTAs leave at once.
 // Then the epoch advances as in epoch_end.  Virtual worlds: the last CTA of
 // the whole grid already follows every rank's CTAs, no stamps needed.
-static __device__ __noinline__ void exit_rank(const FcColl& c, int rank) {
+// `cta_slot`: which slot-1 stamp word carries the exit (0; the FLAT pull path,
+// whose per-CTA slot-1 barrier already used the low indices this call, passes
+// FC_EXIT_CTA_SLOT, an index no grid reaches).
+static __device__ __noinline__ void exit_rank(const FcColl& c, int rank, int cta_slot = 0) {
     __syncthreads();
     if (threadIdx.x != 0) return;
     __threadfence();
@@ -181,11 +184,11 @@ static __device__ __noinline__ void exit_rank(const FcColl& c, int rank) {
         const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
         fence_sys();
         for (int q = 0; q < c.p; ++q)
-            if (q != rank) st_relaxed_sys64(bar_flag(c, q, 1, 0, rank), stamp);
+            if (q != rank) st_relaxed_sys64(bar_flag(c, q, 1, cta_slot, rank), stamp);
         const uint64_t t0 = globaltimer();
         for (int q = 0; q < c.p; ++q) {
             if (q == rank) continue;
-            const uint64_t* f = bar_flag(c, rank, 1, 0, q);
+            const uint64_t* f = bar_flag(c, rank, 1, cta_slot, q);
             uint32_t spins = 0;
             bool good = true;
             while (!reached((uint32_t)ld_relaxed_sys64(f), s_epoch)) {

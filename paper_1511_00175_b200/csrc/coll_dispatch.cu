@@ -89,7 +89,7 @@ int collective_grid(int sched, int arity, int p, bool virt, int op, int64_t n) {
         }
         cap = (int64_t)dev_info().sms * occ;
     }
-    if (cap > FC_MAX_CTAS) cap = FC_MAX_CTAS;
+    if (cap > FC_EXIT_CTA_SLOT) cap = FC_EXIT_CTA_SLOT;  // CTA indices < the reserved exit word
     return (int)cap;
 }
 

@@ -13,7 +13,10 @@ namespace fc {
 // server's sequential order), then either applies SGD and pushes w' to every
 // rank (fused) or pushes the sum to every rank's grad.
 // Pull broadcast (FC_BCAST_PULL): copy every peer's published slice elements
-// produced by the peer CTA with this CTA's index (same grid-stride mapping).
+// produced by the peer CTA with this CTA's index — the per-CTA barrier only
+// orders that CTA's writes, so this must enumerate exactly the element set the
+// data phase gives CTA blockIdx.x (balanced: me + s*G*T for every slab s;
+// c.map_stride: the plain grid stride).
 template <int P, int U>
 __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
@@ -34,19 +37,21 @@ __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
     for (int q = 0; q < P; ++q) src[q] = reinterpret_cast<const float4*>(fused ? w_of(c, q) : grad_of(c, q));
     float4* dst = reinterpret_cast<float4*>(fused ? w_of(c, rank) : grad_of(c, rank));
     const int64_t T = FLAT_T;
-    const int64_t stride = (int64_t)gridDim.x * T * U;
-    for (int64_t rel = (int64_t)blockIdx.x * T * U + threadIdx.x; rel < maxlen; rel += stride) {
+    const int64_t GT = (int64_t)gridDim.x * T;
+    const int64_t me = c.map_stride ? (int64_t)blockIdx.x * T * U + threadIdx.x : (int64_t)blockIdx.x * T + threadIdx.x;
+    const int64_t step = c.map_stride ? T : GT;  // between this thread's U elements of one pass
+    for (int64_t rel = me; rel < maxlen; rel += GT * U) {
         float4 x[U][P];
 #pragma unroll
         for (int j = 0; j < U; ++j)
 #pragma unroll
             for (int q = 0; q < P; ++q)
-                if (q != rank && rel + j * T < len4[q]) x[j][q] = ld_cg(src[q] + b0[q] + rel + j * T);
+                if (q != rank && rel + j * step < len4[q]) x[j][q] = ld_cg(src[q] + b0[q] + rel + j * step);
 #pragma unroll
         for (int j = 0; j < U; ++j)
 #pragma unroll
             for (int q = 0; q < P; ++q)
-                if (q != rank && rel + j * T < len4[q]) st_na(dst + b0[q] + rel + j * T, x[j][q]);
+                if (q != rank && rel + j * step < len4[q]) st_na(dst + b0[q] + rel + j * step, x[j][q]);
     }
     if (blockIdx.x == 0) {  // trailing n % 4 elements of the last slice
         for (int q = 0; q < P; ++q) {
@@ -189,7 +194,11 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     // pull: the same barrier, now BEFORE the broadcast, publishes this CTA's
     // finished results (release after local stores only); then this CTA copies
     // the matching elements of every peer's slice (the ones that peer's CTA
-    // with the same index produced) and the kernel ends with no remote writes.
+    // with the same index produced).  The kernel then still needs the
+    // rank-level exit: peers may be pulling from THIS rank's published slice,
+    // and once the kernel ends the caller may overwrite it (the next backward
+    // writes grad) — without the exit a slow peer reads the new values (found
+    // by the shared-GPU world test, tests/test_multi_gpu.py).
     if (!pull) {
         finish_call(c, rank);
         return;
@@ -197,7 +206,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
     const bool ok2 = cta_barrier(c, rank, 1);
     if (ok && ok2) pull_results<P, U>(c, rank);
     trace(c, 3);
-    epoch_end(c);
+    exit_rank(c, rank, FC_EXIT_CTA_SLOT);
 }
 
 // Kernel table of one unroll factor: flat_kernel<p, arity, U> (arity >= p is

@@ -7,6 +7,7 @@
 
 #define FC_MAX_RANKS 8
 #define FC_MAX_CTAS 1024
+#define FC_EXIT_CTA_SLOT (FC_MAX_CTAS - 1)  // exit stamp word of the FLAT pull path; grids stay below it
 #define FC_MAX_LEVELS 3          // log2(FC_MAX_RANKS)
 #define FC_CHUNK_FLOATS 4096     // flag granularity of the level-structured schedules (16 KB)
 #define FC_BAR_SLOTS 2           // 0 = entry barrier, 1 = exit barrier

@@ -28,11 +28,30 @@ def bits(t):
     return np.ascontiguousarray(t.detach().cpu().numpy(), np.float32).view(np.uint32)
 
 
+def _all_reduce(t, op=None):
+    """all_reduce that also works on the gloo group of a shared-GPU run (CPU staging)."""
+    op = op if op is not None else dist.ReduceOp.SUM
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
+    # FC_MP_GPUS=k: ranks share k GPUs (rank r on GPU r % k) — e.g. an 8-rank world
+    # on a 4-GPU box, exercising the 8-rank kernels and host paths functionally
+    # (co-located ranks time-slice; correctness only, not speed)
+    if os.environ.get("FC_MP_GPUS"):
+        local = local % int(os.environ["FC_MP_GPUS"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if os.environ.get("FC_MP_GPUS"):
+        dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     rank, p = dist.get_rank(), dist.get_world_size()
     sizes = [int(s) for s in os.environ.get("FC_MP_SIZES", "5,16391,1000003").split(",")]
     nmax = max(sizes)
@@ -218,8 +237,8 @@ def main():
     # all ranks hold identical weights
     dg = torch.tensor([int(w[:nmax].view(torch.int32).to(torch.int64).sum().item())], device=dev)
     lo, hi = dg.clone(), dg.clone()
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+    _all_reduce(lo, op=dist.ReduceOp.MIN)
+    _all_reduce(hi, op=dist.ReduceOp.MAX)
     if lo.item() != hi.item():
         fails.append("digest differs across ranks")
     # mismatch test (fresh world): ranks disagree on n -> every rank reports
@@ -266,7 +285,7 @@ def main():
     W3.close()
     dist.barrier()
     nf = torch.tensor([len(fails)], device=dev)
-    dist.all_reduce(nf)
+    _all_reduce(nf)
     if fails:
         print(f"rank {rank} FAILS: {fails}", flush=True)
     if nf.item() == 0 and os.environ.get("FC_MP_TIMEOUT_TEST", "1") == "1":

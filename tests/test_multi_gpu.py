@@ -48,3 +48,24 @@ def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
     assert r.returncode == 0, out[-4000:]
     for k in range(nproc):
         assert f"MP_OK {k}" in out, out[-4000:]
+
+
+def test_eight_rank_world_on_shared_gpus():
+    """The 8-rank kernels and host paths on a real (CUDA-IPC) world even when the
+    box has fewer than 8 GPUs: ranks share the GPUs (rank r on GPU r % k, gloo
+    for the bootstrap).  Co-located ranks time-slice, so this checks values
+    (every schedule, op and the random back-to-back stress, bit-exact vs the
+    oracle) under very different CTA timing, not speed."""
+    k = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if k < 2:
+        pytest.skip("needs >= 2 GPUs")
+    k = min(k, 4)
+    env = dict(os.environ, FC_MP_GPUS=str(k), FC_MP_SIZES="5,16391,300007", FC_MP_STRESS="40",
+               FC_MP_TIMEOUT="30", FC_MP_TIMEOUT_TEST="0", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29618", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    for rank in range(8):
+        assert f"MP_OK {rank}" in out, out[-4000:]
