@@ -920,6 +920,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_TREE_CTAS_PER_SM": "1"},                        # the spill-free tree builds (small-slice default)
     {"FC_FLAT_UNROLL": "1"}, {"FC_FLAT_UNROLL": "2"}, {"FC_FLAT_UNROLL": "4"},  # every FLAT unroll build
     {"FC_EXIT": "rank"}, {"FC_EXIT": "cta"},            # both exit protocols (coll_common.cuh)
+    {"FC_FLAT_MAP": "stride"},                          # the plain grid-stride FLAT work mapping
 ])
 def test_every_kernel_build_bitexact(knobs):
     """The dispatcher picks among several builds of each executor (register
