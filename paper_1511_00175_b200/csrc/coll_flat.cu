@@ -21,8 +21,9 @@ __device__ __forceinline__ const uint16_t* gradh_of(const FcColl& c, int q) {
 
 // 4 elements per unit: 8-byte bf16 loads and float4 weight accesses are both
 // fully coalesced per warp; U units per thread keep (P-1)*8*U remote bytes in
-// flight per thread.
-#define BF16_UNROLL(P) ((P) <= 2 ? 8 : (P) <= 4 ? 4 : 1)
+// flight per thread.  p = 2: U = 6 is spill-free (U = 8 spilled 20 B/thread;
+// measured NiN +2 %, AlexNet -1 % time vs U = 8, scripts/gpu_bf16_unroll.sh).
+#define BF16_UNROLL(P) ((P) <= 2 ? 6 : (P) <= 4 ? 4 : 1)
 __device__ __forceinline__ uint2 ld_cg_u2(const uint2* p) {
     uint2 r;
     asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
