@@ -337,6 +337,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     N = world
+    # FC_BENCH_SHARED_GPUS=k: TEST HOOK ONLY (tests/test_multi_gpu.py) -- rank r runs on GPU
+    # r % k with a gloo group, so the N-rank code path (e.g. N = 8 on a 4-GPU box) can be
+    # exercised end to end.  Co-located ranks time-slice: the line is not a measurement.
+    shared = int(os.environ.get("FC_BENCH_SHARED_GPUS", "0"))
+    if shared:
+        local = local % shared
     if args.gpus != N:
         if N == 1 and args.gpus > 1:
             emit({"error": "run N>1 under torchrun"})
@@ -344,7 +350,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    _coll.gloo = bool(shared)
     fc.load()
     if args.sgd_unroll:
         fc.firecaffe_tune_sgd_unroll(args.sgd_unroll)
@@ -369,7 +379,7 @@ def main():
 
     def dev_barrier():
         if N > 1:
-            dist.all_reduce(tiny)  # device-side rendezvous: kernels start aligned across ranks
+            _all_reduce(tiny)  # device-side rendezvous: kernels start aligned across ranks
             # ~20 us of GPU-side delay, equal on every rank (same clock): the host has
             # enqueued the timed kernel before the GPU reaches the start event, as in a
             # training loop where the allreduce is queued behind the backward pass
@@ -438,12 +448,12 @@ def main():
         ms = [a.elapsed_time(b) for a, b in ev]
         tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
         if N > 1:
-            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+            _all_reduce(tot, dist.ReduceOp.MAX)
         return tot.item() / K, ms, wall
 
     reset()
     restore = (lambda: grad.copy_(g0)) if N > 1 else None  # the tree writes partial sums into grad
-    with clock_sampler(list(range(N)) if (N > 1 and rank == 0) else [local]) as clk:
+    with clock_sampler(sorted({r % (shared or N) for r in range(N)}) if (N > 1 and rank == 0) else [local]) as clk:
         ms_step, ms_list, wall = timed(step, args.steps, args.warmup, pre=restore)
     clocks = clk.summary() if rank == 0 else None
     t = ms_step * 1e-3
@@ -522,9 +532,10 @@ def main():
 
             reset()
             baselines["ps+sgd_ms"] = round(timed(ps_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
-            reset()
-            baselines["nccl_allreduce+sgd_ms"] = round(timed(nccl_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
-            baselines["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
+            if not shared:
+                reset()
+                baselines["nccl_allreduce+sgd_ms"] = round(timed(nccl_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
+                baselines["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
             gb = W.alloc(n, "bf16")  # bf16 gradients on the wire (fp32 accumulate + update)
             gb.copy_(g0.to(torch.bfloat16))
             reset()
@@ -588,11 +599,39 @@ def main():
             "baselines_ms_per_step": baselines,
             "wall_s_timed_region": round(wall, 3),
         }
+        if shared:
+            line["test_hook"] = {"shared_gpus": shared, "note": "ranks time-slice GPUs: not a measurement"}
         emit(line)
     if N > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+class _coll:
+    gloo = False  # set in main(): a gloo group (shared-GPU test hook) stages CUDA tensors via the host
+
+
+def _all_reduce(t, op=None):
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if _coll.gloo and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
+def _all_gather(out, t):
+    import torch.distributed as dist
+    if _coll.gloo and t.is_cuda:
+        oc = [o.cpu() for o in out]
+        dist.all_gather(oc, t.cpu())
+        for o, c in zip(out, oc):
+            o.copy_(c)
+    else:
+        dist.all_gather(out, t)
 
 
 def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W):
@@ -612,7 +651,7 @@ def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, rese
     gs = g0[idx_d].contiguous()
     if N > 1:
         allg = [torch.empty_like(gs) for _ in range(N)]
-        dist.all_gather(allg, gs)
+        _all_gather(allg, gs)
         G = torch.stack(allg).cpu().numpy()
     else:
         G = gs.cpu().numpy()[None, :]
@@ -638,10 +677,10 @@ def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, rese
     dg = torch.tensor([digest], dtype=torch.int64, device=grad.device)
     same = True
     if N > 1:
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        _all_reduce(ok, dist.ReduceOp.MIN)
         dmin, dmax = dg.clone(), dg.clone()
-        dist.all_reduce(dmin, op=dist.ReduceOp.MIN)
-        dist.all_reduce(dmax, op=dist.ReduceOp.MAX)
+        _all_reduce(dmin, dist.ReduceOp.MIN)
+        _all_reduce(dmax, dist.ReduceOp.MAX)
         same = dmin.item() == dmax.item()
     status = W.poll() if W is not None else 0
     return {"bitexact_sampled": bool(ok.item() == 1), "samples": int(idx.numel()), "ranks_identical_digest": same,
