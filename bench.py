@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-steady", action="store_true", help="N=1: skip the > L2 steady-state SGD timing")
     ap.add_argument("--sgd-unroll", type=int, default=0)
     return ap.parse_args()
 
@@ -230,94 +231,113 @@ def time_oracle(n, p, hp, budget_s=10.0, seed=None):
     return el / (steps * m), m, steps
 
 
-def time_oracle_all_cores(n, p, hp, budget_s=5.0):
-    """The same oracle functions, unmodified, called concurrently from one host
-    thread per core on disjoint element slices (the update is elementwise and
-    the ctypes calls release the GIL): SURVEY §8(d)'s "all cores" figure.
-    Returns (seconds per element-step, m, steps, threads)."""
-    import concurrent.futures
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
 
+
+def time_oracle_all_cores(n, p, hp, budget_s=5.0):
+    """The same oracle loops built with -fopenmp (liboracle_omp.so: elements
+    split over every host core, each element's arithmetic and association
+    unchanged -> identical bits, tests/test_oracle.py): SURVEY §8(d)'s "all
+    cores" figure.  Whole world for p > 1 (tree sum of the p ranks' gradients
+    + SGD).  Returns (seconds per element-step, m, steps, threads)."""
     import numpy as np
 
     import fc_inputs
     import oracle
 
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    m = min(n, max(1 << 21, cores << 18))
+    threads = oracle.omp_threads(host_cores())
+    m = min(n, max(1 << 22, threads << 19))
     g = fc_inputs.grads(m, p).numpy() if p > 1 else fc_inputs.grad(m, 0).numpy()[None, :]
     w = fc_inputs.weights(m).numpy()
     v = fc_inputs.momentum(m).numpy()
-    cuts = [m * i // cores for i in range(cores + 1)]
-    sl = [slice(cuts[i], cuts[i + 1]) for i in range(cores) if cuts[i + 1] > cuts[i]]
-
-    def one(s):
-        if p > 1:
-            return oracle.fused_step(g[:, s], w[s], v[s], **hp)
-        return oracle.sgd(w[s], v[s], g[0, s], **hp)
-
     steps, t0 = 0, time.perf_counter()
-    with concurrent.futures.ThreadPoolExecutor(max_workers=len(sl)) as ex:
-        while True:
-            outs = list(ex.map(one, sl))
-            for s_, (wn, vn) in zip(sl, outs):
-                w[s_], v[s_] = wn, vn
-            steps += 1
-            el = time.perf_counter() - t0
-            if el >= budget_s:
-                break
+    while True:
+        if p > 1:
+            w, v = oracle.fused_step(g, w, v, **hp, omp=True)
+        else:
+            w, v = oracle.sgd(w, v, g[0], **hp, omp=True)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
     assert np.isfinite(w).all()
-    return el / (steps * m), m, steps, len(sl)
+    return el / (steps * m), m, steps, threads
+
+
+def cpu_baseline_line(n, N, hp):
+    """cpu_baseline for the JSON line: the oracle on the host cores of this box,
+    computing what the WHOLE N-rank job computes per step (the tree sum of all
+    N ranks' gradients + SGD; N = 1: SGD), on a bounded sample of the workload.
+    `value` is in the line's unit (GB/s of gradient aggregated+applied)."""
+    per_el, m, steps = time_oracle(n, N, hp, budget_s=8.0)
+    what = f"tree sum of {N} ranks' gradients + SGD" if N > 1 else "SGD"
+    cpu = {"value": round(N * 4 / per_el / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+           "sample": f"{steps} whole-world steps ({what}) over the first {m} of {n} params, single-threaded C++ oracle",
+           "ms_per_step_extrapolated": round(per_el * n * 1e3, 3)}
+    pa, ma, sa, ca = time_oracle_all_cores(n, N, hp, budget_s=5.0)
+    cpu["all_cores"] = {"value": round(N * 4 / pa / 1e9, 4), "unit": "GB/s", "cores": ca, "kind": "oracle (OpenMP build)",
+                        "sample": f"{sa} whole-world steps ({what}) over the first {ma} params, the same oracle loops "
+                                  f"built with -fopenmp on {ca} threads",
+                        "ms_per_step_extrapolated": round(pa * n * 1e3, 3)}
+    return cpu
 
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle as it stands, on this box's host
+    cores (the OpenMP build of the same loops, identical bits), computing the
+    whole N-rank job per step (tree sum of N gradients + SGD) on a bounded
+    sample of the workload sized so warmup + steps take about a minute."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    import numpy as np
+
     import fc_inputs
+    import oracle
 
     cfg = fc_inputs.CONFIGS[args.config]
     n, N = cfg["n"], args.gpus
     hp = {k: cfg[k] for k in ("lr", "mu", "wd", "batch")}
-    # calibrate the per-element cost, then size each step's sample so the whole
-    # warmup+steps run takes about 60 s
-    per_el, _, _ = time_oracle(n, N, hp, budget_s=1.0)
+    threads = oracle.omp_threads(host_cores())
+    per_el, _, _, _ = time_oracle_all_cores(n, N, hp, budget_s=1.0)
     total_steps = max(1, args.steps + args.warmup)
     m = int(max(4096, min(n, 60.0 / (total_steps * per_el))))
-    import numpy as np
-
-    import oracle
-
     g = fc_inputs.grads(m, N).numpy() if N > 1 else fc_inputs.grad(m, 0).numpy()[None, :]
     w, v = fc_inputs.weights(m).numpy(), fc_inputs.momentum(m).numpy()
     ts = []
     for k in range(total_steps):
         t0 = time.perf_counter()
         if N > 1:
-            w, v = oracle.fused_step(g, w, v, **hp)
+            w, v = oracle.fused_step(g, w, v, **hp, omp=True)
         else:
-            w, v = oracle.sgd(w, v, g[0], **hp)
+            w, v = oracle.sgd(w, v, g[0], **hp, omp=True)
         if k >= args.warmup:
             ts.append(time.perf_counter() - t0)
     assert np.isfinite(w).all()
     t = sum(ts) / len(ts)
     value = N * 4 * m / t / 1e9
     sample = (f"first {m} of {n} params of every rank's gradient per step "
-              f"({'tree sum of %d ranks + ' % N if N > 1 else ''}SGD), single-threaded C++ oracle")
+              f"({'tree sum of %d ranks + ' % N if N > 1 else ''}SGD), the C++ oracle's loops built with -fopenmp "
+              f"on {threads} host threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
         "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(t * 1e3 * n / m, 3), "ms_per_step_note": "extrapolated to the full n from the sample",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        # the same workload keys as the GPU arm's config (no device-only keys)
-        "config": {"workload": args.config, "n_params": n, "grad_bytes": 4 * n, "ranks": N,
-                   "batch": hp["batch"], "lr": hp["lr"], "mu": hp["mu"], "wd": hp["wd"],
-                   "parallelism": f"dp{N}"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "config": workload_config(args.config, n, N, hp),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
     return 0
+
+
+def workload_config(name, n, N, hp):
+    """The line's `config`: workload keys only (the same on both arms)."""
+    return {"workload": name, "n_params": n, "grad_bytes": 4 * n, "ranks": N, "batch": hp["batch"], "lr": hp["lr"],
+            "mu": hp["mu"], "wd": hp["wd"], "parallelism": f"dp{N}"}
 
 
 # ---------------------------------------------------------------- ours ------
@@ -392,6 +412,7 @@ def main():
             c = W.get_config()
             W.config(args.sched or c["sched"], args.bcast or c["bcast"], 2)
         grad, w, mom = W.alloc(n), W.alloc(n), W.alloc(n)
+        gb = W.alloc(n, "bf16")  # bf16 gradients on the wire (fp32 accumulate + update)
     else:
         W = None
         grad = torch.empty(n, device=dev)
@@ -414,6 +435,10 @@ def main():
 
     # ---- parity spot check (sampled, at full size, in the timed launch configuration)
     parity = parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W)
+    if N > 1:  # every executor, the PS and NCCL baselines and the bf16 wire, same sampled indices
+        parity["executors"] = executor_parity(fc, torch, dist, N, rank, n, hp, grad, w, mom, gb, g0, w0, v0, reset,
+                                              W, nccl=not shared)
+        reset()
 
     # ---- timed region
     def timed(fn, K, Wm, pre=None, cold=True):
@@ -487,6 +512,15 @@ def main():
                 "kernel": "fc::sgd_step_kernel", "alg_bytes_per_launch": alg_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "guide fallback",
                 "frac_of_theoretical_8184": round(achieved / 8184.0, 4)}
+        if roof["traffic"]:
+            roof["traffic_vs_alg"] = round(roof["traffic"] / alg_bytes, 3)
+            if roof["traffic"] < 0.9 * alg_bytes:
+                roof["traffic_note"] = ("ncu dram bytes inside the kernel: the reads are the algorithmic g, w, v; most "
+                                        "of the w', v' writes are still dirty in the 126 MB L2 when the kernel ends "
+                                        "(written back after it), so this frac is L2-assisted -- frac_steady is the "
+                                        "same kernel on a working set > L2")
+        if not args.no_steady and args.config != "vgg19":
+            roof.update(steady_state_sgd(fc, torch, dev, peak, timed, hp))
     else:
         alg_bytes = 2 * (N - 1) / N * 4 * n  # per GPU per direction (allreduce lower bound)
         achieved = alg_bytes / t / 1e9
@@ -536,7 +570,6 @@ def main():
                 reset()
                 baselines["nccl_allreduce+sgd_ms"] = round(timed(nccl_step, Kb, Wb, pre=lambda: grad.copy_(g0))[0], 4)
                 baselines["nccl_version"] = ".".join(map(str, torch.cuda.nccl.version()))
-            gb = W.alloc(n, "bf16")  # bf16 gradients on the wire (fp32 accumulate + update)
             gb.copy_(g0.to(torch.bfloat16))
             reset()
             baselines["flat_bf16_wire_ms"] = round(
@@ -556,16 +589,12 @@ def main():
                 timed(lambda: fc.firecaffe_sgd_step_bf16(w, gb, mom, **hp), Kb, Wb)[0], 4)
 
     # ---- CPU oracle baseline (rank 0, N=1 only)
+    # ---- CPU oracle baseline (rank 0; the whole N-rank job's arithmetic per step)
     cpu = None
-    if rank == 0 and N == 1 and not args.no_cpu_baseline:
-        per_el, m, steps = time_oracle(n, 1, hp, budget_s=10.0)
-        cpu = {"value": round(4 / per_el / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"{steps} SGD steps over the first {m} of {n} params (single-threaded C++ oracle)",
-               "ms_per_step_extrapolated": round(per_el * n * 1e3, 3)}
-        pa, ma, sa, ca = time_oracle_all_cores(n, 1, hp, budget_s=5.0)
-        cpu["all_cores"] = {"value": round(4 / pa / 1e9, 4), "unit": "GB/s", "cores": ca,
-                            "sample": f"{sa} SGD steps over the first {ma} params, the unmodified oracle called "
-                                      f"from {ca} threads on disjoint slices"}
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_line(n, N, hp)
+    if N > 1:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -574,12 +603,10 @@ def main():
             "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded N(0,1)*sigma_seg gradients, 64 log-uniform segments; w~N(0,0.01^2))",
-            "config": {"workload": args.config, "n_params": n, "grad_bytes": 4 * n, "ranks": N,
-                       "batch": hp["batch"], "lr": hp["lr"], "mu": hp["mu"], "wd": hp["wd"],
-                       "step": "firecaffe_sgd_step" if N == 1 else "firecaffe_tree_allreduce_sgd",
-                       "schedule": W.get_config() if W else None,
-                       "l2_flush": "no" if args.no_flush else f"write 512 MiB + read 512 MiB between steps (L2 {l2 >> 20} MiB)",
-                       "parallelism": f"dp{N}"},
+            "config": workload_config(args.config, n, N, hp),
+            "step_api": "firecaffe_sgd_step" if N == 1 else "firecaffe_tree_allreduce_sgd",
+            "executor": W.get_config() if W else None,
+            "l2_flush": "no" if args.no_flush else f"write 512 MiB + read 512 MiB between steps (L2 {l2 >> 20} MiB)",
             "algbw_gbs": round(4 * n / t / 1e9, 2),
             "busbw_gbs": round(4 * n / t / 1e9 * 2 * (N - 1) / N, 2) if N > 1 else None,
             "ms_per_step_median": round(statistics.median(ms_list), 5),
@@ -600,7 +627,13 @@ def main():
             "wall_s_timed_region": round(wall, 3),
         }
         if shared:
+            # ranks time-slice GPUs: the timings are not a measurement, so none are reported
             line["test_hook"] = {"shared_gpus": shared, "note": "ranks time-slice GPUs: not a measurement"}
+            line["valid"] = False
+            for k in ("value", "ms_per_step", "ms_per_step_median", "ms_per_step_warm_l2", "algbw_gbs", "busbw_gbs",
+                      "roofline"):
+                line[k] = None
+            line["e2e"] = None
         emit(line)
     if N > 1:
         dist.barrier()
@@ -632,6 +665,111 @@ def _all_gather(out, t):
             o.copy_(c)
     else:
         dist.all_gather(out, t)
+
+
+def steady_state_sgd(fc, torch, dev, peak, timed, hp):
+    """The 1-GPU fused SGD on a working set larger than L2 (VGG-19 size,
+    BASELINE configs[4]: 3 x 575 MB), timed in the same run and the same way:
+    every byte of w', v' must reach DRAM within the steady state, so this is
+    the kernel's HBM roofline fraction without L2 help."""
+    import fc_inputs
+
+    nv = fc_inputs.CONFIGS["vgg19"]["n"]
+    g = fc_inputs.grad(nv, 0, device=dev)
+    w = fc_inputs.weights(nv, device=dev)
+    v = fc_inputs.momentum(nv, device=dev)
+    ms, _, _ = timed(lambda: fc.firecaffe_sgd_step(w, g, v, **hp), 20, 3)
+    ach = 20 * nv / (ms * 1e-3) / 1e9
+    out = {"frac_steady": round(ach / peak, 4),
+           "steady_state": {"workload": "vgg19", "n_params": nv, "alg_bytes_per_launch": 20 * nv,
+                            "ms_per_launch": round(ms, 5), "achieved": round(ach, 1), "frac": round(ach / peak, 4),
+                            "frac_of_theoretical_8184": round(ach / 8184.0, 4),
+                            "traffic": load_traffic("sgd_step_kernel", "vgg19", 1)}}
+    del g, w, v
+    torch.cuda.empty_cache()
+    return out
+
+
+def executor_parity(fc, torch, dist, N, rank, n, hp, grad, w, mom, gb, g0, w0, v0, reset, W, nccl=True):
+    """Every executor of the fused call (each reaches the oracle's bits through a
+    different schedule), the PS baseline (oracle PS order), the bf16 wire (the
+    oracle on the exactly upcast inputs) -- bit-exact on every rank on the
+    sampled indices -- and the NCCL baseline (order undocumented: the north_star
+    1e-6 tolerance vs the float64 reference, reading R15)."""
+    import numpy as np
+
+    import oracle
+
+    gen = torch.Generator().manual_seed(54321)
+    idx = torch.cat([torch.randint(0, n, (4096,), generator=gen), torch.arange(max(0, n - 64), n)])
+    idx_d = idx.to(grad.device)
+    gs = g0[idx_d].contiguous()
+    allg = [torch.empty_like(gs) for _ in range(N)]
+    _all_gather(allg, gs)
+    G = torch.stack(allg).cpu().numpy()
+    w0s, v0s = w0[idx_d].cpu().numpy(), v0[idx_d].cpu().numpy()
+    w_tree, v_tree = oracle.fused_step(G, w0s, v0s, **hp)
+    s_ps = oracle.ps_sum(G)
+    w_ps, v_ps = oracle.sgd(w0s, v0s, s_ps, **hp)
+    Gb = torch.from_numpy(G).to(torch.bfloat16).float().numpy()
+    w_b, v_b = oracle.fused_step(Gb, w0s, v0s, **hp)
+    s64, a64 = oracle.sum_f64(G), oracle.abs_sum_f64(G)
+    w64, v64 = oracle.sgd_f64(w0s, v0s, s64, **hp)
+
+    def same(t, ref, sel=None):
+        got = t[idx_d].cpu().numpy()
+        if sel is not None:
+            got, ref = got[sel], ref[sel]
+        return bool(np.array_equal(got.view(np.uint32), ref.view(np.uint32)))
+
+    def all_ok(flag):
+        f = torch.tensor([1 if flag else 0], device=grad.device)
+        _all_reduce(f, dist.ReduceOp.MIN)
+        return bool(f.item() == 1)
+
+    out = {}
+    cur = W.get_config()
+    cfgs = [("flat", "direct"), ("flat", "pull"), ("forest", "direct"), ("forest", "tree"), ("single_root", "tree"),
+            ("single_root", "direct")]
+    for sched, bcast in cfgs:
+        if sched == "forest" and (N & (N - 1)):
+            continue
+        W.config(sched, bcast, 2)
+        reset()
+        fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, **hp)
+        torch.cuda.synchronize()
+        b, e = W.owned_range(rank, n)
+        own = ((idx >= b) & (idx < e)).numpy()
+        out[f"{sched}/{bcast}"] = all_ok(same(w, w_tree) and same(mom, v_tree, own))
+    W.config(cur["sched"], cur["bcast"], cur["arity"])
+    reset()
+    fc.firecaffe_ps_allreduce(grad, W)
+    fc.firecaffe_sgd_step(w, grad, mom, **hp)
+    torch.cuda.synchronize()
+    out["ps+sgd"] = all_ok(same(grad, s_ps) and same(w, w_ps) and same(mom, v_ps))
+    reset()
+    gb.copy_(g0.to(torch.bfloat16))
+    fc.firecaffe_tree_allreduce_sgd_bf16(w, gb, mom, world=W, **hp)
+    torch.cuda.synchronize()
+    b, e = W.owned_range(rank, n)
+    own = ((idx >= b) & (idx < e)).numpy()
+    out["flat_bf16_wire"] = all_ok(same(w, w_b) and same(mom, v_b, own))
+    if nccl:
+        reset()
+        dist.all_reduce(grad)
+        fc.firecaffe_sgd_step(w, grad, mom, **hp)
+        torch.cuda.synchronize()
+        S = grad[idx_d].cpu().numpy().astype(np.float64)
+        wg = w[idx_d].cpu().numpy().astype(np.float64)
+        vg = mom[idx_d].cpu().numpy().astype(np.float64)
+        aw, av = np.abs(w0s.astype(np.float64)), np.abs(v0s.astype(np.float64))
+        err_s = float(np.max(np.abs(S - s64) / np.maximum(a64, 1e-30)))
+        ok = (np.all(np.abs(S - s64) <= 1e-6 * a64) and np.all(np.abs(wg - w64) <= 1e-6 * (aw + np.abs(v64)) + 1e-30)
+              and np.all(np.abs(vg - v64) <= 1e-6 * (hp["mu"] * av + hp["lr"] * (a64 / hp["batch"] + hp["wd"] * aw))
+                         + 1e-30))
+        out["nccl_allreduce+sgd"] = {"within_1e-6_of_f64": all_ok(ok), "max_err_sum_over_sum_abs_g": err_s,
+                                     "bitexact_vs_tree_order": all_ok(same(grad, oracle.tree_sum(G, 2)))}
+    return out
 
 
 def parity_check(fc, torch, dist, N, rank, n, hp, grad, w, mom, g0, w0, v0, reset, step, W):

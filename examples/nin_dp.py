@@ -89,9 +89,12 @@ def synthetic_batch(B: int, seed: int, device, classes: int = 10, hw: int = 16):
 
 
 def run(p: int = 4, B: int = 64, steps: int = 5, lr: float = 0.04, mu: float = 0.9, wd: float = 5e-4,
-        sched: str = "flat", bcast: str = "direct"):
+        sched: str = "flat", bcast: str = "direct", capture: list | None = None):
     """Train `steps` iterations with p virtual ranks and, in lockstep, a single-GPU
-    reference.  Returns (per-rank weights list, reference weights, losses)."""
+    reference.  Returns (per-rank weights list, reference weights, losses).
+    `capture` (a list): per step, append a host copy of what the fused call was
+    given and what it produced -- every rank's Σ∇W, and every rank's w and mom
+    after the call -- so a test can recompute the step independently."""
     torch.backends.cudnn.deterministic = True
     torch.backends.cudnn.benchmark = False
     torch.backends.cudnn.allow_tf32 = False  # fp32 convolutions, as Caffe (P:508: fp32 throughout)
@@ -116,7 +119,14 @@ def run(p: int = 4, B: int = 64, steps: int = 5, lr: float = 0.04, mu: float = 0
         shard = B // p
         for r in range(p):  # each worker: sum of the gradients over its sub-batch
             grad_sum_into(replicas[r], x[r * shard:(r + 1) * shard], y[r * shard:(r + 1) * shard], grads[r])
+        if capture is not None:
+            g_in = torch.stack([grads[r] for r in range(p)]).cpu()
         fc.firecaffe_tree_allreduce_sgd_segments(ws[0], grads[0], moms[0], lr, mu, wd, B, segs, W)
+        if capture is not None:
+            capture.append(dict(grads=g_in, w=torch.stack([ws[r] for r in range(p)]).cpu(),
+                                mom=torch.stack([moms[r] for r in range(p)]).cpu(),
+                                owned=[W.owned_range(r, n) for r in range(p)],
+                                segs=(begins, lrm, dm), hp=dict(lr=lr, mu=mu, wd=wd, batch=B)))
         losses.append(float(grad_sum_into(ref, x, y, g_ref)) / B)  # single GPU, whole batch
         fc.firecaffe_sgd_step_segments(w_ref, g_ref, m_ref, lr, mu, wd, B, segs)
     st = W.poll()

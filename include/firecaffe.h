@@ -115,7 +115,12 @@ fc_status firecaffe_heap_export(void* heap, uint8_t* handle_out);
  * firecaffe_world_create: the real world, one process per GPU.
  *   rank, world_size : this process's rank in [0, world_size), world_size in 1..8
  *   cuda_device      : the device this rank uses (must be current on the calling thread)
- *   local_heap       : this rank's heap from firecaffe_heap_alloc (heap_bytes bytes)
+ *   local_heap       : this rank's heap from firecaffe_heap_alloc (heap_bytes bytes);
+ *                      EVERY rank must pass the same heap_bytes: buffers and flags are
+ *                      addressed in a peer's heap at this rank's offsets (the size is
+ *                      part of every collective's call signature, so ranks whose sizes
+ *                      differ fail with FC_ERR_MISMATCH at the entry barrier, whose
+ *                      stamps sit at offsets that do not depend on the size)
  *   handles          : world_size * FC_IPC_HANDLE_BYTES bytes, rank-ordered exports of every
  *                      rank's heap (entry `rank` is ignored); exchanged by the caller
  *                      (e.g. torch.distributed all_gather_object)
@@ -292,14 +297,13 @@ fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
 /* ------------------------------------------------ learning-rate schedules
  * The paper's schedules (R21): FIXED; STEP gamma^floor(iter/stepsize);
  * MULTISTEP gamma^#{steps[k] <= iter} ("reduce this by a factor of 10x twice",
- * P:407); POLY (1 - iter/max_iter)^power (power 0.5).  The factor
- * is evaluated in double (gamma^k by binary powering: k = 1, 2 give gamma and
- * fl(gamma^2); power 0.5 as sqrt, power 1 exactly, other powers via pow), then
- * lr = fl32(base_lr * factor).  firecaffe_lr_at evaluates it on the host;
- * the *_sched entry points below evaluate the same arithmetic on the device.
- * firecaffe_lr_at returns -1 for invalid input (iter < 0, base_lr <= 0 or not
- * finite, stepsize < 1 for STEP, iter > max_iter or max_iter < 1 for POLY,
- * nsteps outside 0..FC_LR_MAX_STEPS, non-finite gamma / power). */
+ * P:407); POLY (1 - it/max_iter)^power with it = min(iter, max_iter) (P:451-452,
+ * power 0.5; past max_iter the schedule stays at its end value, lr = 0 for
+ * power > 0).  The factor is std::pow in double, then lr = fl32(base_lr *
+ * factor) — the oracle's definition, bit for bit.
+ * firecaffe_lr_at returns -1 for invalid input: iter < 0; base_lr <= 0; gamma
+ * <= 0 (STEP, MULTISTEP); power < 0 (POLY); any of them not finite; stepsize
+ * < 1 (STEP); max_iter < 1 (POLY); nsteps outside 0..FC_LR_MAX_STEPS. */
 typedef enum { FC_LR_FIXED = 0, FC_LR_STEP = 1, FC_LR_MULTISTEP = 2, FC_LR_POLY = 3 } fc_lr_policy;
 #define FC_LR_MAX_STEPS 16
 typedef struct {
@@ -315,19 +319,27 @@ typedef struct {
 float firecaffe_lr_at(const fc_lr_schedule* sched, int64_t iter);
 
 /* On-device schedules ("computed on device from an iteration
- * counter, so the step needs no host sync").  An fc_lr_state is a device copy
- * of the schedule plus an iteration counter, on the device current at
- * creation.  firecaffe_sgd_step_sched / firecaffe_tree_allreduce_sgd_sched
- * are firecaffe_sgd_step / firecaffe_tree_allreduce_sgd with lr =
- * firecaffe_lr_at(sched, iter) computed by the kernel from the counter, which
- * the same kernel then advances by one (stream-ordered): a captured CUDA
- * graph replays the training step with the schedule moving on, no host
- * involvement.  POLY at iter >= max_iter gives lr = 0.  A call that enqueues
- * nothing (n = 0) does not advance the counter.  Collective rule: every rank
- * creates its state from the same schedule and first_iter and makes the same
- * calls (the schedule, not the iteration, is part of the call signature).
+ * counter, so the step needs no host sync").  An fc_lr_state holds, on the
+ * device current at creation, the schedule's lr at every level it can reach
+ * (computed once by firecaffe_lr_at's arithmetic on the host: the number of
+ * decays for STEP / MULTISTEP, the clamped iteration for POLY; a STEP table
+ * ends where gamma^k has become 0 or inf in fp32, after which the value
+ * cannot change) plus an iteration counter.  firecaffe_sgd_step_sched /
+ * firecaffe_tree_allreduce_sgd_sched are firecaffe_sgd_step /
+ * firecaffe_tree_allreduce_sgd with lr = firecaffe_lr_at(sched, iter), read by
+ * the kernel from that table at the counter, which the same kernel then
+ * advances by one (stream-ordered): a captured CUDA graph replays the training
+ * step with the schedule moving on, no host involvement, and device and host
+ * give identical bits.  A call that enqueues nothing (n = 0) does not advance
+ * the counter.  Collective rule: every rank creates its state from the same
+ * schedule and first_iter and makes the same calls (the schedule, not the
+ * iteration, is part of the call signature).
  *   firecaffe_lr_state_create   first_iter >= 0; FC_ERR_INVALID_ARG for an
- *                               invalid schedule (as firecaffe_lr_at)
+ *                               invalid schedule (as firecaffe_lr_at);
+ *                               FC_ERR_UNSUPPORTED if the table would exceed
+ *                               2^24 levels (POLY max_iter >= 2^24, or a STEP
+ *                               gamma so close to 1 that gamma^k needs more
+ *                               levels to reach 0 in fp32)
  *   firecaffe_lr_state_get_iter synchronous: waits for the device, then reads
  *   firecaffe_lr_state_set_iter synchronous: waits for the device, then writes
  *                               (resume from a checkpoint)

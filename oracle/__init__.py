@@ -31,27 +31,36 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
 CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
 
 _lib = None
+_lib_omp = None
 
 
 def build(force: bool = False) -> str:
-    """Compile oracle.cpp -> liboracle.so with gcc (no GPU, no CUDA)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + ".tmp%d" % os.getpid()
-        subprocess.check_call(["g++", *CFLAGS, "-o", tmp, _SRC])
-        os.replace(tmp, _LIB)
+    """Compile oracle.cpp -> liboracle.so (single-threaded, the correctness
+    oracle) and, from the same file with -fopenmp, liboracle_omp.so (the same
+    loops with their elements split over the host cores; identical bits) with
+    gcc (no GPU, no CUDA)."""
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+            tmp = out + ".tmp%d" % os.getpid()
+            subprocess.check_call(["g++", *CFLAGS, *extra, "-o", tmp, _SRC])
+            os.replace(tmp, out)
     return _LIB
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(omp: bool = False):
+    """The oracle library (omp=True: the OpenMP build of the same source)."""
+    global _lib, _lib_omp
+    if (_lib_omp if omp else _lib) is None:
         build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_LIB_OMP if omp else _LIB)
         P, I, I64, F = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float
         L.oracle_version.restype = I
+        L.oracle_threads.restype = I
+        L.oracle_set_threads.argtypes = [I]
         L.oracle_tree_sum.argtypes = [P, I, I64, I, P]
         L.oracle_ps_sum.argtypes = [P, I, I64, P]
         L.oracle_sgd.argtypes = [P, P, P, I64, F, F, F, I64]
@@ -65,8 +74,11 @@ def lib():
         for f in ("oracle_tree_sum", "oracle_ps_sum", "oracle_sgd", "oracle_sum_f64",
                   "oracle_abs_sum_f64", "oracle_sgd_f64", "oracle_tree_plan", "oracle_sgd_segments"):
             getattr(L, f).restype = I
-        _lib = L
-    return _lib
+        if omp:
+            _lib_omp = L
+        else:
+            _lib = L
+    return _lib_omp if omp else _lib
 
 
 def _f32(a) -> np.ndarray:
@@ -83,12 +95,13 @@ def _check(rc: int, what: str):
         raise ValueError(f"oracle {what}: invalid arguments (rc={rc})")
 
 
-def tree_sum(g, k: int = 2) -> np.ndarray:
-    """Reduction-tree sum of g[p, n] with branching factor k."""
+def tree_sum(g, k: int = 2, omp: bool = False) -> np.ndarray:
+    """Reduction-tree sum of g[p, n] with branching factor k.
+    omp=True: the OpenMP build (elements over the host cores; same bits)."""
     g = _f32(g)
     p, n = g.shape
     out = np.empty(n, np.float32)
-    _check(lib().oracle_tree_sum(_ptr(g), p, n, k, _ptr(out)), "tree_sum")
+    _check(lib(omp).oracle_tree_sum(_ptr(g), p, n, k, _ptr(out)), "tree_sum")
     return out
 
 
@@ -101,14 +114,14 @@ def ps_sum(g) -> np.ndarray:
     return out
 
 
-def sgd(w, v, S, lr: float, mu: float, wd: float, batch: int):
+def sgd(w, v, S, lr: float, mu: float, wd: float, batch: int, omp: bool = False):
     """One Caffe-convention SGD step; returns new (w', v') arrays."""
     w = _f32(w).copy()
     v = _f32(v).copy()
     S = _f32(S)
     n = w.shape[0]
     assert v.shape == (n,) and S.shape == (n,)
-    _check(lib().oracle_sgd(_ptr(w), _ptr(v), _ptr(S), n, lr, mu, wd, batch), "sgd")
+    _check(lib(omp).oracle_sgd(_ptr(w), _ptr(v), _ptr(S), n, lr, mu, wd, batch), "sgd")
     return w, v
 
 
@@ -178,9 +191,17 @@ def tree_plan(p: int, k: int = 2):
     return [(buf[3 * e], buf[3 * e + 1], buf[3 * e + 2]) for e in range(m)]
 
 
-def fused_step(g, w, v, lr: float, mu: float, wd: float, batch: int, k: int = 2):
+def fused_step(g, w, v, lr: float, mu: float, wd: float, batch: int, k: int = 2, omp: bool = False):
     """The whole hot path for one iteration: tree sum, then one SGD step
     (the sum is what a single GPU would compute; P:121 update).
     Every rank ends with the same (w', v')."""
-    S = tree_sum(g, k)
-    return sgd(w, v, S, lr, mu, wd, batch)
+    S = tree_sum(g, k, omp=omp)
+    return sgd(w, v, S, lr, mu, wd, batch, omp=omp)
+
+
+def omp_threads(threads: int = 0) -> int:
+    """Threads the OpenMP build uses (threads > 0: set it first)."""
+    L = lib(True)
+    if threads > 0:
+        L.oracle_set_threads(int(threads))
+    return int(L.oracle_threads())

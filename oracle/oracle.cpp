@@ -29,7 +29,13 @@
 // (one rounding), emulation through double is NOT (SURVEY.md §0 finding 6).
 // x86-64 evaluates float arithmetic in float (SSE, FLT_EVAL_METHOD == 0), so
 // every `+`, `*`, `-` below is one IEEE round-to-nearest-even fp32 operation.
-// Everything is single-threaded, no FTZ/DAZ (MXCSR default).
+// No FTZ/DAZ (MXCSR default).  liboracle.so (the correctness oracle) is
+// single-threaded.  The element loops of oracle_tree_sum and oracle_sgd carry
+// `#pragma omp` directives that the plain build ignores; the -fopenmp build of
+// this same file (liboracle_omp.so, bench.py's all-cores CPU baseline,
+// SURVEY §8(d)) splits ELEMENTS over the host cores.  Every element's
+// arithmetic and association is unchanged, so both builds give identical bits
+// (tests/test_oracle.py checks it).
 
 #include <cmath>
 #include <cstdint>
@@ -40,6 +46,15 @@ extern "C" {
 
 // Version tag so tests can check they loaded the intended build.
 int oracle_version(void) { return 1; }
+
+#ifdef _OPENMP
+#include <omp.h>
+int oracle_threads(void) { return omp_get_max_threads(); }
+void oracle_set_threads(int t) { if (t > 0) omp_set_num_threads(t); }
+#else
+int oracle_threads(void) { return 1; }
+void oracle_set_threads(int) {}
+#endif
 
 // ---------------------------------------------------------------------------
 // Reduction tree sum (Eq. 4; Fig. P:312-315).
@@ -62,7 +77,10 @@ int oracle_version(void) { return 1; }
 // ---------------------------------------------------------------------------
 int oracle_tree_sum(const float* g, int p, int64_t n, int k, float* out) {
     if (p < 1 || n < 0 || k < 2 || (n > 0 && (!g || !out))) return 1;
+#pragma omp parallel
+    {
     std::vector<float> part((size_t)p);
+#pragma omp for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         for (int r = 0; r < p; ++r) part[(size_t)r] = g[(int64_t)r * n + i];
         int64_t step = 1;
@@ -78,6 +96,7 @@ int oracle_tree_sum(const float* g, int p, int64_t n, int k, float* out) {
             step *= k;
         }
         out[i] = part[0];
+    }
     }
     return 0;
 }
@@ -114,6 +133,7 @@ int oracle_sgd(float* w, float* v, const float* S, int64_t n, float lr, float mu
                float wd, int64_t batch) {
     if (n < 0 || batch < 1 || (n > 0 && (!w || !v || !S))) return 1;
     const float inv_b = 1.0f / (float)batch;
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
         const float g = S[i] * inv_b;
         const float d = std::fma(wd, w[i], g);
@@ -167,28 +187,33 @@ int oracle_sgd_segments(float* w, float* v, const float* S, int64_t n, float lr,
 //   policy 1 step       : base_lr · gamma^floor(iter / stepsize)
 //   policy 2 multistep  : base_lr · gamma^#{k : steps[k] <= iter}   ("reduce this by
 //                          a factor of 10x twice")
-//   policy 3 poly       : base_lr · (1 − iter/max_iter)^power      (power 0.5)
-// Evaluated in double, rounded once to fp32 (reading R21).  Returns -1 on
-// invalid arguments (iter < 0, poly with iter > max_iter, stepsize < 1, ...).
+//   policy 3 poly       : base_lr · (1 − it/max_iter)^power,  it = min(iter, max_iter)
+//                          (power 0.5; past max_iter training has ended and
+//                          the schedule stays at its end value — reading R21)
+// Evaluated in double (std::pow), rounded once to fp32 (reading R21).  Domain:
+// base_lr > 0, gamma > 0, power >= 0 (all finite), stepsize >= 1, max_iter >= 1,
+// iter >= 0; returns -1 otherwise.
 // ---------------------------------------------------------------------------
 float oracle_lr_at(int policy, float base_lr, int64_t iter, float gamma, int64_t stepsize,
                    const int64_t* steps, int nsteps, float power, int64_t max_iter) {
-    if (iter < 0 || !(base_lr > 0.0f)) return -1.0f;
+    if (iter < 0 || !(base_lr > 0.0f) || !std::isfinite(base_lr)) return -1.0f;
     double f = 1.0;
     if (policy == 0) {
         f = 1.0;
     } else if (policy == 1) {
-        if (stepsize < 1) return -1.0f;
+        if (stepsize < 1 || !(gamma > 0.0f) || !std::isfinite(gamma)) return -1.0f;
         f = std::pow((double)gamma, (double)(iter / stepsize));
     } else if (policy == 2) {
-        if (nsteps < 0 || (nsteps > 0 && !steps)) return -1.0f;
+        if (nsteps < 0 || (nsteps > 0 && !steps) || !(gamma > 0.0f) || !std::isfinite(gamma))
+            return -1.0f;
         int k = 0;
         for (int j = 0; j < nsteps; ++j)
             if (steps[j] <= iter) ++k;
         f = std::pow((double)gamma, (double)k);
     } else if (policy == 3) {
-        if (max_iter < 1 || iter > max_iter) return -1.0f;
-        f = std::pow(1.0 - (double)iter / (double)max_iter, (double)power);
+        if (max_iter < 1 || !(power >= 0.0f) || !std::isfinite(power)) return -1.0f;
+        const int64_t it = iter < max_iter ? iter : max_iter;
+        f = std::pow(1.0 - (double)it / (double)max_iter, (double)power);
     } else {
         return -1.0f;
     }

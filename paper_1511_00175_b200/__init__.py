@@ -45,40 +45,62 @@ def _stream(stream) -> int:
     return stream if isinstance(stream, int) else stream.cuda_stream
 
 
-def _numel(n, x):
-    return x.numel() if n is None else int(n)
+def _numel(n, x, *more, world=None):
+    """The element count n (default: x.numel()), checked before any library call:
+    every tensor argument must hold at least n elements (bf16 gradients and host
+    buffers included) and every CUDA buffer must sit on one device -- the
+    world's, for collective calls.  The C ABI takes plain pointers and cannot
+    check sizes, so a short buffer would otherwise be read or written out of
+    bounds on the device."""
+    if n is None:
+        if isinstance(x, int):
+            raise ValueError("n is required when buffers are raw pointers")
+        n = x.numel()
+    n = int(n)
+    dev = world.device if world is not None else None
+    for t in (x, *more):
+        if t is None or isinstance(t, int):
+            continue
+        if t.numel() < n:
+            raise ValueError(f"buffer of {t.numel()} elements is shorter than n = {n}")
+        if t.is_cuda:
+            if dev is None:
+                dev = t.device.index
+            elif t.device.index != dev:
+                raise ValueError(f"buffer on cuda:{t.device.index}, expected cuda:{dev}")
+    return n
 
 
 def firecaffe_sgd_step(w, grad, mom, lr: float, mu: float, wd: float, batch: int, n=None, stream=None):
     """One fused SGD step on one GPU, in place on w and mom (header: firecaffe_sgd_step)."""
-    check(load().firecaffe_sgd_step(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd, int(batch),
+    check(load().firecaffe_sgd_step(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom), lr, mu, wd, int(batch),
                                     _stream(stream)), "firecaffe_sgd_step")
 
 
 def firecaffe_tree_allreduce(grad, world: "World", n=None, stream=None):
     """In-place reduction-tree sum over all ranks (header: firecaffe_tree_allreduce)."""
-    check(load().firecaffe_tree_allreduce(_ptr(grad), _numel(n, grad), world.handle, _stream(stream)),
+    check(load().firecaffe_tree_allreduce(_ptr(grad), _numel(n, grad, world=world), world.handle, _stream(stream)),
           "firecaffe_tree_allreduce")
 
 
 def firecaffe_tree_allreduce_sgd(w, grad, mom, lr: float, mu: float, wd: float, batch: int,
                                  world: "World", n=None, stream=None):
     """Tree sum fused with the SGD update and the weight broadcast."""
-    check(load().firecaffe_tree_allreduce_sgd(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd,
+    check(load().firecaffe_tree_allreduce_sgd(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom, world=world), lr, mu, wd,
                                               int(batch), world.handle, _stream(stream)),
           "firecaffe_tree_allreduce_sgd")
 
 
 def firecaffe_ps_allreduce(grad, world: "World", n=None, stream=None):
     """The paper's parameter server (baseline): rank 0 sums ascending, all receive."""
-    check(load().firecaffe_ps_allreduce(_ptr(grad), _numel(n, grad), world.handle, _stream(stream)),
+    check(load().firecaffe_ps_allreduce(_ptr(grad), _numel(n, grad, world=world), world.handle, _stream(stream)),
           "firecaffe_ps_allreduce")
 
 
 def firecaffe_allgather_owned(buf, world: "World", n=None, stream=None):
     """Copy every rank's owned slice of a symmetric buffer to all ranks (checkpoint the
     sharded momentum)."""
-    check(load().firecaffe_allgather_owned(_ptr(buf), _numel(n, buf), world.handle, _stream(stream)),
+    check(load().firecaffe_allgather_owned(_ptr(buf), _numel(n, buf, world=world), world.handle, _stream(stream)),
           "firecaffe_allgather_owned")
 
 
@@ -138,14 +160,14 @@ class Segments:
 
 def firecaffe_sgd_step_segments(w, grad, mom, lr, mu, wd, batch, segs: Segments, n=None, stream=None):
     """firecaffe_sgd_step with Caffe per-blob multipliers."""
-    check(load().firecaffe_sgd_step_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd, int(batch),
+    check(load().firecaffe_sgd_step_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom), lr, mu, wd, int(batch),
                                              segs.handle, _stream(stream)), "firecaffe_sgd_step_segments")
 
 
 def firecaffe_tree_allreduce_sgd_segments(w, grad, mom, lr, mu, wd, batch, segs: Segments, world: "World",
                                           n=None, stream=None):
     """firecaffe_tree_allreduce_sgd with Caffe per-blob multipliers."""
-    check(load().firecaffe_tree_allreduce_sgd_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr, mu, wd,
+    check(load().firecaffe_tree_allreduce_sgd_segments(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom, world=world), lr, mu, wd,
                                                        int(batch), segs.handle, world.handle, _stream(stream)),
           "firecaffe_tree_allreduce_sgd_segments")
 
@@ -163,14 +185,14 @@ def _bptr(x) -> int:
 
 def firecaffe_sgd_step_bf16(w, grad_bf16, mom, lr, mu, wd, batch, segs=None, n=None, stream=None):
     """firecaffe_sgd_step with a bf16 gradient (exact upcast)."""
-    check(load().firecaffe_sgd_step_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w), lr, mu, wd, int(batch),
+    check(load().firecaffe_sgd_step_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w, grad_bf16, mom), lr, mu, wd, int(batch),
                                          segs.handle if segs else None, _stream(stream)), "firecaffe_sgd_step_bf16")
 
 
 def firecaffe_tree_allreduce_sgd_bf16(w, grad_bf16, mom, lr, mu, wd, batch, world: "World", segs=None, n=None,
                                       stream=None):
     """The fused tree allreduce + SGD with bf16 gradients on the wire."""
-    check(load().firecaffe_tree_allreduce_sgd_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w), lr, mu, wd,
+    check(load().firecaffe_tree_allreduce_sgd_bf16(_ptr(w), _bptr(grad_bf16), _ptr(mom), _numel(n, w, grad_bf16, mom, world=world), lr, mu, wd,
                                                    int(batch), segs.handle if segs else None, world.handle,
                                                    _stream(stream)), "firecaffe_tree_allreduce_sgd_bf16")
 
@@ -186,7 +208,7 @@ def _hptr(x) -> int:
 def firecaffe_sgd_step_host(w, grad, mom, grad_host, w_host, lr, mu, wd, batch, segs=None, n=None, stream=None):
     """firecaffe_sgd_step fed from pinned host memory, pipelined H2D || SGD || D2H."""
     check(load().firecaffe_sgd_step_host(_ptr(w), _ptr(grad), _ptr(mom), _hptr(grad_host), _hptr(w_host),
-                                         _numel(n, w), lr, mu, wd, int(batch), segs.handle if segs else None,
+                                         _numel(n, w, grad, mom, grad_host, w_host), lr, mu, wd, int(batch), segs.handle if segs else None,
                                          _stream(stream)), "firecaffe_sgd_step_host")
 
 
@@ -194,8 +216,8 @@ def firecaffe_tree_allreduce_sgd_host(w, grad, mom, grad_host, w_host, lr, mu, w
                                       segs=None, n=None, stream=None):
     """firecaffe_tree_allreduce_sgd with the gradient from / weights to pinned host memory."""
     check(load().firecaffe_tree_allreduce_sgd_host(_ptr(w), _ptr(grad), _ptr(mom), _hptr(grad_host),
-                                                   _hptr(w_host), _numel(n, w), lr, mu, wd, int(batch),
-                                                   segs.handle if segs else None, world.handle, _stream(stream)),
+                                                   _hptr(w_host), _numel(n, w, grad, mom, grad_host, w_host, world=world), lr, mu, wd,
+                                                   int(batch), segs.handle if segs else None, world.handle, _stream(stream)),
           "firecaffe_tree_allreduce_sgd_host")
 
 
@@ -259,7 +281,7 @@ class LrState:
 
 def firecaffe_sgd_step_sched(w, grad, mom, lr: LrState, mu, wd, batch, segs=None, n=None, stream=None):
     """firecaffe_sgd_step with lr from the device-resident schedule (advanced by one)."""
-    check(load().firecaffe_sgd_step_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr.handle, mu, wd,
+    check(load().firecaffe_sgd_step_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom), lr.handle, mu, wd,
                                           int(batch), segs.handle if segs else None, _stream(stream)),
           "firecaffe_sgd_step_sched")
 
@@ -267,6 +289,6 @@ def firecaffe_sgd_step_sched(w, grad, mom, lr: LrState, mu, wd, batch, segs=None
 def firecaffe_tree_allreduce_sgd_sched(w, grad, mom, lr: LrState, mu, wd, batch, world: "World", segs=None,
                                        n=None, stream=None):
     """firecaffe_tree_allreduce_sgd with lr from the device-resident schedule (advanced by one)."""
-    check(load().firecaffe_tree_allreduce_sgd_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w), lr.handle, mu,
+    check(load().firecaffe_tree_allreduce_sgd_sched(_ptr(w), _ptr(grad), _ptr(mom), _numel(n, w, grad, mom, world=world), lr.handle, mu,
                                                     wd, int(batch), segs.handle if segs else None, world.handle,
                                                     _stream(stream)), "firecaffe_tree_allreduce_sgd_sched")

@@ -8,6 +8,7 @@
 
 #include <cmath>
 #include <mutex>
+#include <vector>
 
 #include "fc_internal.h"
 #include "fc_launch.h"
@@ -27,6 +28,7 @@ struct fc_segments {
 
 struct fc_lr_state {
     FcLrDev* d;         // device copy of the schedule + the iteration counter
+    float* table;       // device: the lr of every schedule level (FcLrDev::table)
     fc_lr_schedule s;   // host copy (validation, call signature)
     int device;
     uint32_t hash;      // of the schedule: part of the collective call signature
@@ -128,17 +130,19 @@ static float inv_batch(int64_t batch) {
     return one / b;
 }
 
-// Exit protocol of the collectives (coll_common.cuh): rank-level (default: the
-// last CTA per GPU does one sys fence + stamp exchange) or, with FC_EXIT=cta,
-// the per-CTA exit barrier.  Measured (scripts/gpu_exit_sweep.sh,
-// profiles/r01_sweep_exit_*): 1-4 us faster per call up to NiN size, equal at
-// AlexNet size.  Part of the call signature, so ranks that disagree fail with
-// FC_ERR_MISMATCH at entry instead of waiting on stamps that never come.
+// Exit protocol of the collectives (coll_common.cuh exit_rank): rank-level,
+// the last CTA per GPU does one sys fence and writes its stamp into its own
+// heap, peers poll it over NVLink (default, FC_EXIT=poll); the same with the
+// stamps pushed into the peers' heaps (FC_EXIT=push, round 1's default); or,
+// with FC_EXIT=cta, the per-CTA exit barrier.  Measured in
+// profiles/r01_sweep_exit_* (cta vs push) and profiles/r02_* (push vs poll).
+// Part of the call signature, so ranks that disagree fail with FC_ERR_MISMATCH
+// at entry instead of waiting on stamps that never come.
 static int exit_mode() {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("FC_EXIT");
-        m = (e && strcmp(e, "cta") == 0) ? 0 : 1;
+        m = (e && strcmp(e, "cta") == 0) ? 0 : (e && (strcmp(e, "push") == 0 || strcmp(e, "rank") == 0)) ? 1 : 2;
     }
     return m;
 }
@@ -517,6 +521,10 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
         mix(&c.off_grad, sizeof c.off_grad);
         mix(&c.off_w, sizeof c.off_w);
         mix(&c.off_mom, sizeof c.off_mom);
+        // the flag layout (red/av offsets) derives from each rank's own heap size and
+        // is applied to the peers' heaps: ranks whose heaps differ must fail at the
+        // entry barrier (its stamps sit at fixed offsets) before any such flag is used
+        mix(&w->heap_bytes, sizeof w->heap_bytes);
         c.sig = h;
     }
     c.op = op;
@@ -890,28 +898,84 @@ fc_status firecaffe_tree_allreduce_sgd_host(float* w, float* grad, float* mom,
     return cudaStreamWaitEvent(user, world->hp_start, 0) == cudaSuccess ? FC_OK : FC_ERR_CUDA;
 }
 
-// The paper's learning-rate schedules: fc_lr_factor
-// (fc_internal.h), the same arithmetic the *_sched kernels evaluate on the
-// device, one rounding to fp32 (R21).
+// The paper's learning-rate schedules, R21:
+// STEP gamma^floor(iter/stepsize), MULTISTEP gamma^#{steps <= iter}, POLY
+// (1 - min(iter, max_iter)/max_iter)^power; the factor in double by std::pow,
+// lr = one rounding of base_lr * factor to fp32.  Domain: base_lr > 0, gamma > 0,
+// power >= 0 (all finite), stepsize >= 1, max_iter >= 1, 0 <= nsteps <= 16.
 static bool valid_schedule(const fc_lr_schedule* s) {
     if (!s || !(s->base_lr > 0.0f) || !std::isfinite(s->base_lr)) return false;
     switch (s->policy) {
         case FC_LR_FIXED:
             return true;
         case FC_LR_STEP:
-            return s->stepsize >= 1 && std::isfinite(s->gamma);
+            return s->stepsize >= 1 && s->gamma > 0.0f && std::isfinite(s->gamma);
         case FC_LR_MULTISTEP:
-            return s->nsteps >= 0 && s->nsteps <= FC_LR_MAX_STEPS && std::isfinite(s->gamma);
+            return s->nsteps >= 0 && s->nsteps <= FC_LR_MAX_STEPS && s->gamma > 0.0f &&
+                   std::isfinite(s->gamma);
         case FC_LR_POLY:
-            return s->max_iter >= 1 && std::isfinite(s->power);
+            return s->max_iter >= 1 && s->power >= 0.0f && std::isfinite(s->power);
     }
     return false;
 }
 
+// lr of schedule level k (FcLrDev, fc_internal.h): STEP / MULTISTEP k = the
+// number of decays so far, POLY k = the (clamped) iteration, FIXED k = 0.
+static float lr_of_level(const fc_lr_schedule& s, int64_t k) {
+    double f = 1.0;
+    if (s.policy == FC_LR_STEP || s.policy == FC_LR_MULTISTEP)
+        f = std::pow((double)s.gamma, (double)k);
+    else if (s.policy == FC_LR_POLY)
+        f = std::pow(1.0 - (double)k / (double)s.max_iter, (double)s.power);
+    return (float)((double)s.base_lr * f);
+}
+
+static int64_t level_of(const fc_lr_schedule& s, int64_t iter) {
+    switch (s.policy) {
+        case FC_LR_STEP: return iter / s.stepsize;
+        case FC_LR_MULTISTEP: {
+            int64_t k = 0;
+            for (int j = 0; j < s.nsteps; ++j) k += s.steps[j] <= iter;
+            return k;
+        }
+        case FC_LR_POLY: return iter < s.max_iter ? iter : s.max_iter;
+    }
+    return 0;
+}
+
 float firecaffe_lr_at(const fc_lr_schedule* s, int64_t iter) {
     if (!valid_schedule(s) || iter < 0) return -1.0f;
-    if (s->policy == FC_LR_POLY && iter > s->max_iter) return -1.0f;
-    return fc_lr_value(*s, iter);
+    return lr_of_level(*s, level_of(*s, iter));
+}
+
+// Largest level table an fc_lr_state uploads (64 MB).
+#define FC_LR_MAX_LEVELS ((int64_t)1 << 24)
+
+// Every level's lr, host-computed (lr_of_level).  STEP: the levels are
+// unbounded, but gamma^k is monotone, so once the fp32 value is 0 (gamma < 1)
+// or inf (gamma > 1), or gamma == 1, every later level has the same value and
+// the device clamps to the last entry.
+static fc_status lr_levels(const fc_lr_schedule& s, std::vector<float>* out) {
+    out->clear();
+    switch (s.policy) {
+        case FC_LR_FIXED: out->push_back(s.base_lr); return FC_OK;
+        case FC_LR_MULTISTEP:
+            for (int64_t k = 0; k <= s.nsteps; ++k) out->push_back(lr_of_level(s, k));
+            return FC_OK;
+        case FC_LR_POLY:
+            if (s.max_iter + 1 > FC_LR_MAX_LEVELS) return FC_ERR_UNSUPPORTED;
+            out->resize((size_t)s.max_iter + 1);
+            for (int64_t k = 0; k <= s.max_iter; ++k) (*out)[(size_t)k] = lr_of_level(s, k);
+            return FC_OK;
+        case FC_LR_STEP:
+            for (int64_t k = 0;; ++k) {
+                if (k >= FC_LR_MAX_LEVELS) return FC_ERR_UNSUPPORTED;
+                const float v = lr_of_level(s, k);
+                out->push_back(v);
+                if (s.gamma == 1.0f || v == 0.0f || std::isinf(v)) return FC_OK;
+            }
+    }
+    return FC_ERR_INVALID_ARG;
 }
 
 fc_status firecaffe_lr_state_create(const fc_lr_schedule* sched, int64_t first_iter,
@@ -919,21 +983,38 @@ fc_status firecaffe_lr_state_create(const fc_lr_schedule* sched, int64_t first_i
     if (!out) return FC_ERR_INVALID_ARG;
     *out = nullptr;
     if (!valid_schedule(sched) || first_iter < 0) return FC_ERR_INVALID_ARG;
+    fc_lr_schedule s = *sched;
+    if (s.policy != FC_LR_MULTISTEP) s.nsteps = 0;
+    for (int j = s.nsteps; j < FC_LR_MAX_STEPS; ++j) s.steps[j] = 0;
+    std::vector<float> levels;
+    fc_status st = lr_levels(s, &levels);
+    if (st != FC_OK) return st;
     fc_lr_state* t = new fc_lr_state();
     memset(t, 0, sizeof(*t));
-    t->s = *sched;
-    if (t->s.policy != FC_LR_MULTISTEP) t->s.nsteps = 0;
-    for (int j = t->s.nsteps; j < FC_LR_MAX_STEPS; ++j) t->s.steps[j] = 0;
+    t->s = s;
     uint32_t h = 2166136261u;
     const unsigned char* b = (const unsigned char*)&t->s;
     for (size_t i = 0; i < sizeof(t->s); ++i) h = (h ^ b[i]) * 16777619u;
     t->hash = h;
     FcLrDev init;
     memset(&init, 0, sizeof(init));
-    init.s = t->s;
+    init.policy = s.policy;
+    init.nsteps = s.nsteps;
+    init.stepsize = s.stepsize;
+    init.max_iter = s.max_iter;
+    for (int j = 0; j < FC_LR_MAX_STEPS; ++j) init.steps[j] = s.steps[j];
+    init.nlevels = (int64_t)levels.size();
     init.iter = first_iter;
-    if (cudaGetDevice(&t->device) != cudaSuccess || cudaMalloc(&t->d, sizeof(FcLrDev)) != cudaSuccess ||
-        cudaMemcpy(t->d, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) {
+    const size_t tb = levels.size() * sizeof(float);
+    if (cudaGetDevice(&t->device) != cudaSuccess || cudaMalloc(&t->table, tb) != cudaSuccess ||
+        cudaMemcpy(t->table, levels.data(), tb, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMalloc(&t->d, sizeof(FcLrDev)) != cudaSuccess) {
+        cudaGetLastError();
+        firecaffe_lr_state_destroy(t);
+        return FC_ERR_CUDA;
+    }
+    init.table = t->table;
+    if (cudaMemcpy(t->d, &init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) {
         cudaGetLastError();
         firecaffe_lr_state_destroy(t);
         return FC_ERR_CUDA;
@@ -945,6 +1026,7 @@ fc_status firecaffe_lr_state_create(const fc_lr_schedule* sched, int64_t first_i
 fc_status firecaffe_lr_state_destroy(fc_lr_state* t) {
     if (!t) return FC_OK;
     if (t->d) cudaFree(t->d);
+    if (t->table) cudaFree(t->table);
     delete t;
     return FC_OK;
 }

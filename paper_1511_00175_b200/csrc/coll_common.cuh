@@ -22,10 +22,10 @@ constexpr int FLAT_T = kFlatThreads;              // threads per CTA (FLAT / PS)
 // float4 per thread per operand in flight in FLAT: enough remote bytes in flight
 // (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
 // (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*).
-// p >= 7: U = 1 — U = 2 needs more than the 128 registers a 512-thread CTA
-// allows and spills 84-140 B/thread (ptxas -v), while U = 1 still keeps
-// 148 x 512 x 6..7 x 16 B = 7-8.5 MB in flight per GPU.
-#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : (P) <= 6 ? 2 : 1)
+// p >= 6: U = 1 — U = 2 needs more than the 128 registers a 512-thread CTA
+// allows and spills 96-140 B/thread (ptxas -v), while U = 1 still keeps
+// 148 x 512 x 5..7 x 16 B = 6-8.5 MB in flight per GPU.
+#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : (P) <= 5 ? 2 : 1)
 constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
 constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
 static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
@@ -78,7 +78,7 @@ __shared__ float s_lr;
 __device__ __forceinline__ void epoch_begin(const FcColl& c) {
     if (threadIdx.x == 0) {
         s_epoch = *(volatile uint32_t*)c.ctl + 1u;
-        s_lr = c.lrs ? fc_lr_value(c.lrs->s, *(volatile int64_t*)&c.lrs->iter) : c.lr;
+        s_lr = c.lrs ? fc_lr_dev(c.lrs) : c.lr;
     }
     __syncthreads();
 }
@@ -156,43 +156,65 @@ static __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
     return __syncthreads_and(good) != 0;
 }
 
-// Rank-level exit (c.rank_exit = 1): instead of an all-to-all barrier per CTA
-// (every CTA paying a sys-scope fence; the fence gets slower the more CTAs
+// Rank-level exit (c.rank_exit = 1 or 2): instead of an all-to-all barrier per
+// CTA (every CTA paying a sys-scope fence; the fence gets slower the more CTAs
 // issue it), every CTA orders its writes — local and peer — with a gpu-scope
 // fence and arrives on the call's CTA counter (ctl[1]); the LAST CTA to arrive
-// on this GPU makes all of them visible system-wide with ONE sys fence, stamps
-// every peer's exit word and waits for every peer's stamp (written by that
+// on this GPU makes all of them visible system-wide with ONE sys fence and
+// writes its exit stamp, then waits for every peer's stamp (written by that
 // peer's last CTA after all of ITS CTAs arrived).  When the kernel ends, every
 // store any peer made into this rank's heap has landed.  Memory-model chain
 // (PTX causality order is transitive): CTA stores -> fence.gpu + counter
 // increment -> last CTA's increment + fence.gpu (same GPU) -> fence.sys +
 // stamp -> the peer's acquire.sys of the stamp.  The other CTAs leave at once.
+// Where the stamp goes:
+//   1 (push): into every peer's heap; each rank polls its own heap (local
+//     loads).  The stamps are remote stores issued after the fence, and a
+//     kernel that ends with remote stores in flight waits ~4 us longer to
+//     complete (scripts/gap_bench.cu: 9.7 vs 5.8 us).
+//   2 (poll, default): into the rank's OWN heap; the last CTA's threads q < p
+//     poll peer q's stamp word over NVLink with acquire loads, in parallel.
+//     No remote store follows the fence, so the kernel completes like one
+//     that only wrote locally.
 // Then the epoch advances as in epoch_end.  Virtual worlds: the last CTA of
 // the whole grid already follows every rank's CTAs, no stamps needed.
 // `cta_slot`: which slot-1 stamp word carries the exit (0; the FLAT pull path,
 // whose per-CTA slot-1 barrier already used the low indices this call, passes
 // FC_EXIT_CTA_SLOT, an index no grid reaches).
-static __device__ __noinline__ void exit_rank(const FcColl& c, int rank, int cta_slot = 0) {
+__shared__ uint32_t s_last;
+static __device__ __forceinline__ void exit_rank(const FcColl& c, int rank, int cta_slot = 0) {
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    __threadfence();
-    const uint32_t total = gridDim.x * gridDim.y;
-    const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
-    if (done != total) return;
-    __threadfence();
+    const int t = threadIdx.x;
+    if (t == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * gridDim.y;
+        s_last = atomicAdd(c.ctl + 1, 1u) + 1u == total;
+    }
+    __syncthreads();
+    if (!s_last) return;
     if (c.rank >= 0) {
         const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
-        fence_sys();
-        for (int q = 0; q < c.p; ++q)
-            if (q != rank) st_relaxed_sys64(bar_flag(c, q, 1, cta_slot, rank), stamp);
-        const uint64_t t0 = globaltimer();
-        for (int q = 0; q < c.p; ++q) {
-            if (q == rank) continue;
-            const uint64_t* f = bar_flag(c, rank, 1, cta_slot, q);
+        const bool poll = c.rank_exit == 2;
+        if (t == 0) {
+            __threadfence();
+            fence_sys();
+            if (poll) {
+                st_relaxed_sys64(bar_flag(c, rank, 1, cta_slot, rank), stamp);
+            } else {
+                for (int q = 0; q < c.p; ++q)
+                    if (q != rank) st_relaxed_sys64(bar_flag(c, q, 1, cta_slot, rank), stamp);
+            }
+        }
+        if (poll) __syncthreads();  // thread q polls only after the fence and the own stamp
+        bool good = true;
+        if (t < c.p && t != rank) {
+            // poll: peer t's own stamp word in ITS heap (remote acquire loads);
+            // push: the word peer t wrote into this rank's heap (local loads)
+            const uint64_t* f = poll ? bar_flag(c, t, 1, cta_slot, t) : bar_flag(c, rank, 1, cta_slot, t);
+            const uint64_t t0 = globaltimer();
             uint32_t spins = 0;
-            bool good = true;
-            while (!reached((uint32_t)ld_relaxed_sys64(f), s_epoch)) {
-                if ((++spins & 63u) == 0) {
+            while (!reached((uint32_t)(poll ? ld_acquire_sys64(f) : ld_relaxed_sys64(f)), s_epoch)) {
+                if ((++spins & (poll ? 7u : 63u)) == 0) {
                     if (*(volatile int*)c.status != FC_OK) { good = false; break; }
                     if (globaltimer() - t0 > c.timeout_ns) {
                         atomicCAS(c.status, FC_OK, FC_ERR_TIMEOUT);
@@ -201,14 +223,16 @@ static __device__ __noinline__ void exit_rank(const FcColl& c, int rank, int cta
                     }
                 }
             }
-            if (!good) break;
-            (void)ld_acquire_sys64(f);
+            if (good && !poll) (void)ld_acquire_sys64(f);
         }
+        __syncthreads();
     }
-    c.ctl[1] = 0u;
-    advance_lr(c);
-    __threadfence();
-    atomicExch(c.ctl, s_epoch);
+    if (t == 0) {
+        c.ctl[1] = 0u;
+        advance_lr(c);
+        __threadfence();
+        atomicExch(c.ctl, s_epoch);
+    }
 }
 
 // End of a collective whose data phase may have written into peers' heaps:

@@ -35,7 +35,7 @@ __device__ __forceinline__ float4 bf16x4_to_f32(const uint2 u) {
 }
 
 template <int P, int K>
-__global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
+__global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const __grid_constant__ FcColl c) {
     constexpr int U = BF16_UNROLL(P);
     const int rank = my_rank(c);
     epoch_begin(c);
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const FcColl c) {
 // buffer (off_grad) to every other rank, so all ranks end with the full vector
 // (e.g. the sharded momentum of the fused update, for a checkpoint: R18).
 template <int P>
-__global__ void __launch_bounds__(FLAT_T) allgather_kernel(const FcColl c) {
+__global__ void __launch_bounds__(FLAT_T) allgather_kernel(const __grid_constant__ FcColl c) {
     const int rank = my_rank(c);
     epoch_begin(c);
     trace(c, 0);

@@ -71,7 +71,7 @@ __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
 }
 
 template <int P, int K, int U>
-__global__ void __launch_bounds__(FLAT_T) flat_kernel(const FcColl c) {
+__global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ FcColl c) {
     const int rank = my_rank(c);
     const bool pull = c.bcast == FC_BCAST_PULL && c.op != FC_OP_PS;
     epoch_begin(c);

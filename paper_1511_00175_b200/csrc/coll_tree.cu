@@ -10,7 +10,7 @@ namespace fc {
 
 // ------------------------------------------------------------ FOREST -------
 template <int P, int MINB>
-__global__ void __launch_bounds__(TREE_T, MINB) forest_kernel(const FcColl c) {
+__global__ void __launch_bounds__(TREE_T, MINB) forest_kernel(const __grid_constant__ FcColl c) {
     constexpr int M = (P >= 8) ? 3 : (P >= 4) ? 2 : (P >= 2) ? 1 : 0;
     static_assert((1 << M) == P, "forest needs a power-of-two world");
     const int rank = my_rank(c);
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(TREE_T, MINB) forest_kernel(const FcColl c) {
 // The paper's binomial tree rooted at rank 0: level l, rank r with
 // r % 2^(l+1) == 0 absorbs the whole partial of r + 2^l (if < p).
 template <int P, int MINB>
-__global__ void __launch_bounds__(TREE_T, MINB) single_root_kernel(const FcColl c) {
+__global__ void __launch_bounds__(TREE_T, MINB) single_root_kernel(const __grid_constant__ FcColl c) {
     const int rank = my_rank(c);
     const int G = gridDim.x, b = blockIdx.x;
     const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;

@@ -44,60 +44,46 @@ struct FcSegs {
     int nseg;
 };
 
-#ifdef __CUDACC__
-#define FC_HD __host__ __device__
-#else
-#define FC_HD
-#endif
-
-// Learning-rate factor of the paper's schedules at iteration `iter` (DESIGN.md
-// R21), the same arithmetic on the host (firecaffe_lr_at) and on the device
-// (the *_sched entry points): STEP / MULTISTEP gamma^k by binary powering in
-// double (k = 1, 2: gamma, fl(gamma^2)); POLY (1 - iter/max_iter)^power in
-// double, power 0.5 (the paper's) as the correctly rounded sqrt, power
-// 1 as the base itself, others through pow; 0 at and after max_iter.  The
-// caller validates the schedule.
-FC_HD inline double fc_lr_factor(const fc_lr_schedule& s, int64_t iter) {
-    int64_t k = 0;
-    switch (s.policy) {
-        case FC_LR_STEP:
-            k = iter / s.stepsize;
-            break;
-        case FC_LR_MULTISTEP:
-            for (int j = 0; j < s.nsteps; ++j) k += s.steps[j] <= iter;
-            break;
-        case FC_LR_POLY: {
-            if (iter >= s.max_iter) return 0.0;
-            const double x = 1.0 - (double)iter / (double)s.max_iter;
-            if (s.power == 0.5f) return sqrt(x);
-            if (s.power == 1.0f) return x;
-            return pow(x, (double)s.power);
-        }
-        default:
-            return 1.0;
-    }
-    double f = 1.0, b = (double)s.gamma;
-    while (k > 0) {
-        if (k & 1) f *= b;
-        k >>= 1;
-        if (k) b *= b;
-    }
-    return f;
-}
-
-// fl32(base_lr * factor): one rounding of the double product to fp32
-FC_HD inline float fc_lr_value(const fc_lr_schedule& s, int64_t iter) {
-    return (float)((double)s.base_lr * fc_lr_factor(s, iter));
-}
-
-// Device-resident schedule state of the *_sched entry points: the schedule,
-// the iteration the next call uses, and the CTA arrival counter with which the
-// last CTA of a call advances `iter` (stream order publishes it to the next call).
+// Device-resident schedule state of the *_sched entry points (R21).
+// The learning rate the schedule gives at every reachable "level" is computed
+// ONCE on the host, by the same definition the oracle writes (factor by
+// std::pow in double, one rounding of base_lr * factor to fp32), and uploaded
+// as a table; the kernels only map the iteration to its level and load the
+// fp32 value, so host and device give identical bits for every valid schedule.
+//   FIXED      level 0
+//   STEP       level floor(iter / stepsize)          (table ends where the value
+//   MULTISTEP  level #{steps[j] <= iter}              stops changing: 0, inf, or
+//   POLY       level min(iter, max_iter)              gamma == 1; clamped beyond)
+// `iter` is the iteration the next call uses; `done` is the CTA arrival counter
+// with which the last CTA of a call advances it (stream order publishes it).
 struct FcLrDev {
-    fc_lr_schedule s;
+    int policy;
+    int nsteps;
+    int64_t stepsize;
+    int64_t max_iter;
+    int64_t steps[FC_LR_MAX_STEPS];
+    const float* table;  // device: lr of level 0 .. nlevels-1
+    int64_t nlevels;
     int64_t iter;
     uint32_t done;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float fc_lr_dev(const FcLrDev* d) {
+    const int64_t it = *(volatile const int64_t*)&d->iter;
+    int64_t k = 0;
+    switch (d->policy) {
+        case FC_LR_STEP: k = it / d->stepsize; break;
+        case FC_LR_MULTISTEP:
+            for (int j = 0; j < d->nsteps; ++j) k += d->steps[j] <= it;
+            break;
+        case FC_LR_POLY: k = it < d->max_iter ? it : d->max_iter; break;
+        default: k = 0;
+    }
+    if (k >= d->nlevels) k = d->nlevels - 1;
+    return d->table[k];
+}
+#endif
 
 // Everything a collective kernel needs to find every rank's buffers.
 struct FcPeers {

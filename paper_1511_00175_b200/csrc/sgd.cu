@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) sgd_step_kernel(float4* __restrict__ w4,
                                                        FcLrDev* lrs) {
     if (lrs) {  // firecaffe_sgd_step_sched: the schedule at its current iteration
         __shared__ float s_lr;
-        if (threadIdx.x == 0) s_lr = fc_lr_value(lrs->s, *(volatile int64_t*)&lrs->iter);
+        if (threadIdx.x == 0) s_lr = fc_lr_dev(lrs);
         __syncthreads();
         lr = s_lr;
     }

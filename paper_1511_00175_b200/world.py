@@ -103,20 +103,39 @@ class World:
         self.p = dist.get_world_size(group)
         self.heap_bytes = int(heap_bytes)
         heap = ctypes.c_void_p()
-        check(L.firecaffe_heap_alloc(self.heap_bytes, ctypes.byref(heap)), "firecaffe_heap_alloc")
-        self.heap = heap.value
-        try:
-            hbuf = (ctypes.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
-            check(L.firecaffe_heap_export(self.heap, hbuf), "firecaffe_heap_export")
-            handles = exchange_handles(bytes(hbuf), group, self.heap_bytes)
-            allh = (ctypes.c_uint8 * (_lib.FC_IPC_HANDLE_BYTES * self.p)).from_buffer_copy(b"".join(handles))
-            w = ctypes.c_void_p()
-            check(L.firecaffe_world_create(self.rank, self.p, self.device, self.heap, allh, self.heap_bytes,
-                                           int(timeout_s * 1e9), ctypes.byref(w)), "firecaffe_world_create")
-        except BaseException:
-            L.firecaffe_heap_free(self.heap)  # no leaked heap on a failed bootstrap
-            self.heap = None
-            raise
+        st = L.firecaffe_heap_alloc(self.heap_bytes, ctypes.byref(heap))
+        self.heap = heap.value if st == _lib.FC_OK else None
+        err = None if st == _lib.FC_OK else f"firecaffe_heap_alloc: {_lib.status_str(st)}"
+        w = ctypes.c_void_p()
+        if err is None:
+            try:
+                hbuf = (ctypes.c_uint8 * _lib.FC_IPC_HANDLE_BYTES)()
+                check(L.firecaffe_heap_export(self.heap, hbuf), "firecaffe_heap_export")
+                handles = exchange_handles(bytes(hbuf), group, self.heap_bytes)
+                allh = (ctypes.c_uint8 * (_lib.FC_IPC_HANDLE_BYTES * self.p)).from_buffer_copy(b"".join(handles))
+                check(L.firecaffe_world_create(self.rank, self.p, self.device, self.heap, allh, self.heap_bytes,
+                                               int(timeout_s * 1e9), ctypes.byref(w)), "firecaffe_world_create")
+            except Exception as e:  # noqa: BLE001 -- reported to every rank below
+                err = str(e)
+        else:
+            # the others still exchange handles: take part so nobody waits forever
+            try:
+                exchange_handles(bytes(_lib.FC_IPC_HANDLE_BYTES), group, self.heap_bytes)
+            except Exception:  # noqa: BLE001
+                pass
+        # every rank learns whether EVERY rank succeeded; on any failure all of
+        # them tear down (no rank keeps a mapping of a peer heap that was freed,
+        # none is left waiting in a later collective)
+        oks = [None] * self.p
+        dist.all_gather_object(oks, err, group=group)
+        bad = [(r, e) for r, e in enumerate(oks) if e is not None]
+        if bad:
+            if w.value:
+                L.firecaffe_world_destroy(w.value)
+            if self.heap:
+                L.firecaffe_heap_free(self.heap)
+                self.heap = None
+            raise RuntimeError("world creation failed on rank(s) " + "; ".join(f"{r}: {e}" for r, e in bad))
         self.handle = w.value
         self.layout = SymmetricLayout(self.heap_bytes, L.firecaffe_heap_reserved_bytes(self.heap_bytes))
         dist.barrier(group)  # every peer has mapped every heap before any collective runs

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--sleep", type=int, default=400_000, help="GPU cycles of delay before the pre-stamp")
     ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush (warm L2: code, flags, data)")
+    ap.add_argument("--dump", action="store_true", help="also report the slowest CTAs of the last iteration")
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -105,8 +106,16 @@ def main():
                 r["data_end_max_us"] = (tr[:, 2].max().item() - first) / 1e3
                 r["start_skew_us"] = (tr[:, 0].max().item() - first) / 1e3
                 r["pre_stamp_abs"] = t[0]
+                de = sorted(((tr[:, 2] - first).double() / 1e3).tolist())
+                q = lambda f: de[min(len(de) - 1, int(f * len(de)))]
+                r["data_end_p10_us"], r["data_end_p25_us"], r["data_end_p75_us"], r["data_end_p90_us"] = \
+                    q(0.10), q(0.25), q(0.75), q(0.90)
+                if args.dump and it == args.iters + 2:
+                    r["_slowest_ctas"] = torch.argsort(tr[:, 2], descending=True)[:12].tolist()
             rows.append(r)
-        med = {k: round(statistics.median([r[k] for r in rows]), 2) for k in rows[0]}
+        med = {k: round(statistics.median([r[k] for r in rows]), 2) for k in rows[0] if not k.startswith("_")}
+        if "_slowest_ctas" in rows[-1]:
+            med["slowest_ctas_last_iter"] = rows[-1]["_slowest_ctas"]
         allm = [None] * p
         dist.all_gather_object(allm, med)
         out[case] = allm

@@ -88,6 +88,35 @@ def main():
             b, e = W.owned_range(rank, n)
             if not np.array_equal(bits(mom[b:e]), v_ref[b:e].view(np.uint32)):
                 fails.append(f"fused mom {sched}/{bcast} n={n}")
+        # NCCL baseline ("existing library support"): NCCL's
+        # allreduce order is undocumented, so it is held to the north_star
+        # tolerance against the float64 left-to-right reference (reading R15):
+        # |S - S64| <= 1e-6 * sum|g|; w', v' scaled likewise (tests/test_oracle.py)
+        if dist.get_backend() == "nccl":
+            grad[:n].copy_(g_all[rank])
+            w[:n].copy_(w0)
+            mom[:n].copy_(v0)
+            dist.all_reduce(grad[:n])
+            fc.firecaffe_sgd_step(w, grad, mom, n=n, **HP)
+            torch.cuda.synchronize()
+            ga = g_all.numpy()
+            s64, a64 = oracle.sum_f64(ga), oracle.abs_sum_f64(ga)
+            w64, v64 = oracle.sgd_f64(w0.numpy(), v0.numpy(), s64, **HP)
+            gs = grad[:n].cpu().numpy().astype(np.float64)
+            wg = w[:n].cpu().numpy().astype(np.float64)
+            vg = mom[:n].cpu().numpy().astype(np.float64)
+            w0d, v0d = np.abs(w0.numpy().astype(np.float64)), np.abs(v0.numpy().astype(np.float64))
+            tol_v = 1e-6 * (HP["mu"] * v0d + HP["lr"] * (a64 / HP["batch"] + HP["wd"] * w0d)) + 1e-30
+            if not np.all(np.abs(gs - s64) <= 1e-6 * a64):
+                fails.append(f"nccl sum n={n}: max err/sum|g| {np.max(np.abs(gs - s64) / np.maximum(a64, 1e-30)):.3g}")
+            if not np.all(np.abs(wg - w64) <= 1e-6 * (w0d + np.abs(v64)) + 1e-30):
+                fails.append(f"nccl+sgd w n={n}")
+            if not np.all(np.abs(vg - v64) <= tol_v):
+                fails.append(f"nccl+sgd mom n={n}")
+            if rank == 0:
+                print(f"NCCL_TOL n={n} max|S-S64|/sum|g| = {np.max(np.abs(gs - s64) / np.maximum(a64, 1e-30)):.3g} "
+                      f"bitexact_vs_tree={np.array_equal(grad[:n].cpu().numpy().view(np.uint32), s_ref.view(np.uint32))}",
+                      flush=True)
         # parameter server
         grad[:n].copy_(g_all[rank])
         fc.firecaffe_ps_allreduce(grad, W, n=n)
@@ -283,6 +312,35 @@ def main():
         fails.append("grid-mismatched call modified data")
     W4.close()
     W3.close()
+    # ranks create their worlds with different heap sizes (a C client that skips the
+    # Python bootstrap's check): the flag layout would differ, so the call signature
+    # (which covers heap_bytes) must make every rank fail before any flag is used
+    import ctypes
+
+    from paper_1511_00175_b200 import _lib as fl
+    L = fl.load()
+    hb = heap_bytes_for(4096 + 4096) + (2 << 20)
+    hp_ = ctypes.c_void_p()
+    assert L.firecaffe_heap_alloc(hb, ctypes.byref(hp_)) == 0
+    hbuf = (ctypes.c_uint8 * fl.FC_IPC_HANDLE_BYTES)()
+    assert L.firecaffe_heap_export(hp_.value, hbuf) == 0
+    from paper_1511_00175_b200.world import exchange_handles
+    hs = exchange_handles(bytes(hbuf))
+    allh = (ctypes.c_uint8 * (fl.FC_IPC_HANDLE_BYTES * p)).from_buffer_copy(b"".join(hs))
+    w5 = ctypes.c_void_p()
+    claimed = hb - (1 << 20) if rank == 1 else hb
+    assert L.firecaffe_world_create(rank, p, local, hp_.value, allh, claimed, int(5e9), ctypes.byref(w5)) == 0
+    reserved = L.firecaffe_heap_reserved_bytes(hb)
+    buf5 = hp_.value + (reserved + 255) // 256 * 256
+    dist.barrier()
+    torch.cuda.synchronize()
+    L.firecaffe_tree_allreduce(buf5, 1000, w5.value, torch.cuda.current_stream().cuda_stream)
+    st5 = L.firecaffe_world_poll(w5.value)
+    if st5 != 3:
+        fails.append(f"heap-size mismatch: expected FC_ERR_MISMATCH, got {st5}")
+    dist.barrier()
+    L.firecaffe_world_destroy(w5.value)
+    L.firecaffe_heap_free(hp_.value)
     dist.barrier()
     nf = torch.tensor([len(fails)], device=dev)
     _all_reduce(nf)

@@ -100,9 +100,7 @@ def test_lr_schedules_match_oracle(policy, kw):
     import oracle
 
     for base in (0.01, 0.04, 0.08):
-        for it in [0, 1, 999, 1000, 99_999, 100_000, 150_000, 200_000, 449_999, 450_000]:
-            if policy == "poly" and it > kw["max_iter"]:
-                continue
+        for it in [0, 1, 999, 1000, 99_999, 100_000, 150_000, 200_000, 449_999, 450_000, 450_001, 10**9]:
             assert fc.firecaffe_lr_at(policy, base, it, **kw) == oracle.lr_at(policy, base, it, **kw)
 
 
@@ -113,10 +111,9 @@ def test_lr_schedules_match_oracle(policy, kw):
     ("step", 0.04, dict(gamma=0.5, stepsize=10), range(0, 2_000)),
 ])
 def test_lr_schedules_dense_bitexact(policy, base, kw, iters):
-    """The library's schedule arithmetic (fc_lr_factor: binary powering, sqrt for
-    power 0.5; the same code the *_sched kernels run on the device) gives the
-    oracle's lr (std::pow) bit for bit at every sampled iteration of the paper's
-    schedules."""
+    """firecaffe_lr_at gives the oracle's lr bit for bit at every sampled
+    iteration of the paper's schedules (the device reads a table of exactly
+    these values, tests/test_gpu_parity.py)."""
     import oracle
 
     bad = [it for it in iters
@@ -124,35 +121,47 @@ def test_lr_schedules_dense_bitexact(policy, base, kw, iters):
     assert not bad, f"{len(bad)} iterations differ, first {bad[:5]}"
 
 
-def test_lr_schedules_random_within_one_ulp():
-    """Schedules outside the paper's (gamma^k with k >= 3, arbitrary powers): the
-    binary powering / pow of the library may differ from the oracle's std::pow
-    in the last bit of the double; after the fp32 rounding they agree to 1 ulp
-    (and almost always exactly)."""
+def _random_schedules(rng, count):
+    """Random valid schedules well outside the paper's (gamma^k for large k,
+    arbitrary powers, gamma > 1, iterations past max_iter)."""
+    for _ in range(count):
+        base = float(np.float32(10 ** rng.uniform(-4, -0.5)))
+        u = rng.random()
+        if u < 0.35:
+            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 1.2))), stepsize=int(rng.integers(1, 50)))
+            yield "step", base, kw, rng.integers(0, 5_000, 40)
+        elif u < 0.5:
+            steps = tuple(sorted(int(x) for x in rng.integers(0, 3_000, int(rng.integers(0, 17)))))
+            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 0.99))), steps=steps)
+            yield "multistep", base, kw, rng.integers(0, 4_000, 40)
+        else:
+            kw = dict(power=float(np.float32(rng.uniform(0.0, 3.0))), max_iter=int(rng.integers(1, 100_000)))
+            yield "poly", base, kw, rng.integers(0, kw["max_iter"] + 10, 40)
+
+
+def test_lr_schedules_random_bitexact():
+    """Every valid schedule, not only the paper's: firecaffe_lr_at (the host
+    arithmetic that also fills the device table) equals the oracle's lr bit for
+    bit -- no ulp allowance (R21)."""
     import oracle
 
     rng = np.random.default_rng(151100175)
-    exact = total = 0
-    for _ in range(300):
-        base = float(np.float32(10 ** rng.uniform(-4, -0.5)))
-        if rng.random() < 0.5:
-            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 0.99))), stepsize=int(rng.integers(1, 50)))
-            policy, its = "step", rng.integers(0, 2_000, 20)
-        else:
-            kw = dict(power=float(np.float32(rng.uniform(0.1, 3.0))), max_iter=int(rng.integers(10, 100_000)))
-            policy, its = "poly", rng.integers(0, kw["max_iter"] + 1, 20)
+    total = 0
+    for policy, base, kw, its in _random_schedules(rng, 400):
         for it in its:
             a = np.float32(fc.firecaffe_lr_at(policy, base, int(it), **kw))
             b = np.float32(oracle.lr_at(policy, base, int(it), **kw))
             total += 1
-            exact += a == b
-            assert abs(int(a.view(np.int32)) - int(b.view(np.int32))) <= 1, (policy, base, kw, it, a, b)
-    assert exact >= 0.99 * total
+            assert a.view(np.uint32) == b.view(np.uint32), (policy, base, kw, int(it), a, b)
+    assert total == 400 * 40
 
 
 def test_lr_schedule_errors():
+    assert fc.firecaffe_lr_at("poly", 0.01, 11, max_iter=10) == 0.0  # clamped at max_iter (R21)
     with pytest.raises(ValueError):
-        fc.firecaffe_lr_at("poly", 0.01, 11, max_iter=10)
+        fc.firecaffe_lr_at("poly", 0.01, 3, power=-1.0, max_iter=10)
+    with pytest.raises(ValueError):
+        fc.firecaffe_lr_at("step", 0.01, 3, gamma=0.0, stepsize=2)
     with pytest.raises(ValueError):
         fc.firecaffe_lr_at("step", 0.01, 5, stepsize=0)
     with pytest.raises(ValueError):
@@ -219,7 +228,9 @@ def test_lr_state_argument_errors_without_gpu():
     bad = [fc._schedule("poly", 0.01, 0.1, 0, (), 0.5, 0),      # max_iter < 1
            fc._schedule("step", 0.01, 0.1, 0, (), 0.5, 0),      # stepsize < 1
            fc._schedule("fixed", -0.01, 0.1, 0, (), 0.5, 0),    # base_lr <= 0
-           fc._schedule("step", 0.01, float("nan"), 5, (), 0.5, 0)]
+           fc._schedule("step", 0.01, float("nan"), 5, (), 0.5, 0),
+           fc._schedule("step", 0.01, -0.5, 5, (), 0.5, 0),       # gamma <= 0
+           fc._schedule("poly", 0.01, 0.1, 0, (), -1.0, 10)]     # power < 0
     for s in bad:
         assert L.firecaffe_lr_state_create(ctypes.byref(s), 0, ctypes.byref(out)) == _lib.FC_ERR_INVALID_ARG
         assert not out.value

@@ -498,9 +498,7 @@ LR_CASES = [
 
 
 def _lr_ref(policy, base, it, kw):
-    """The oracle's lr; the device gives 0 at and after a poly max_iter (header)."""
-    if policy == "poly" and it >= kw["max_iter"]:
-        return 0.0
+    """The oracle's lr (past a poly max_iter the schedule stays at its end, R21)."""
     return oracle.lr_at(policy, base, it, **kw)
 
 
@@ -564,6 +562,66 @@ def test_virtual_fused_sched_bitexact(p, sched, bcast, policy, base, kw):
     finally:
         st.close()
         W.close()
+
+
+def test_device_lr_table_random_schedules_bitexact():
+    """The device's lr at every iteration equals the oracle's, bit for bit, for
+    random valid schedules well outside the paper's (gamma^k up to thousands of
+    decays, gamma > 1, arbitrary poly powers, iterations past max_iter): with
+    S = 1, B = 1, w = v = 0, wd = mu = 0 one sched step leaves mom = fl(lr * 1)
+    = lr exactly, so mom[0] after each call IS the lr the kernel used."""
+    rng = np.random.default_rng(20151100)
+    one = torch.ones(4, device="cuda")
+    w, v = torch.zeros(4, device="cuda"), torch.zeros(4, device="cuda")
+    checked = 0
+    for _ in range(120):
+        base = float(np.float32(10 ** rng.uniform(-4, -0.5)))
+        u = rng.random()
+        if u < 0.4:
+            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 1.2))), stepsize=int(rng.integers(1, 40)))
+            policy = "step"
+        elif u < 0.55:
+            steps = tuple(sorted(int(x) for x in rng.integers(0, 300, int(rng.integers(0, 17)))))
+            kw = dict(gamma=float(np.float32(rng.uniform(0.05, 0.99))), steps=steps)
+            policy = "multistep"
+        else:
+            kw = dict(power=float(np.float32(rng.uniform(0.0, 3.0))), max_iter=int(rng.integers(1, 400)))
+            policy = "poly"
+        first, K = int(rng.integers(0, 300)), 12
+        st = fc.LrState(policy, base, first_iter=first, **kw)
+        log = torch.empty(K, device="cuda")
+        try:
+            for k in range(K):
+                fc.firecaffe_sgd_step_sched(w, one, v, st, mu=0.0, wd=0.0, batch=1)
+                log[k] = v[0]
+            got = log.cpu().numpy()
+        finally:
+            st.close()
+        want = np.array([oracle.lr_at(policy, base, it, **kw) for it in range(first, first + K)], np.float32)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (policy, base, kw, first, got, want)
+        checked += K
+    assert checked == 120 * 12
+
+
+def test_device_lr_table_long_step_schedule():
+    """A STEP schedule whose table is long (gamma = 0.999: ~100 k levels until
+    gamma^k is 0 in fp32) and iterations far past the table's end (clamped to
+    the last level, where the value can no longer change)."""
+    kw = dict(gamma=float(np.float32(0.999)), stepsize=1)
+    one = torch.ones(4, device="cuda")
+    w, v = torch.zeros(4, device="cuda"), torch.zeros(4, device="cuda")
+    for first in (0, 5_000, 99_000, 10**6, 10**12):
+        st = fc.LrState("step", 0.04, first_iter=first, **kw)
+        try:
+            log = torch.empty(3, device="cuda")
+            for k in range(3):
+                fc.firecaffe_sgd_step_sched(w, one, v, st, mu=0.0, wd=0.0, batch=1)
+                log[k] = v[0]
+            got = log.cpu().numpy()
+        finally:
+            st.close()
+        want = np.array([oracle.lr_at("step", 0.04, it, **kw) for it in range(first, first + 3)], np.float32)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (first, got, want)
 
 
 def test_cuda_graph_replays_the_schedule():
@@ -919,7 +977,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_TREE_CTAS_PER_SM": "2"},                        # the 128-register tree builds (large-slice default)
     {"FC_TREE_CTAS_PER_SM": "1"},                        # the spill-free tree builds (small-slice default)
     {"FC_FLAT_UNROLL": "1"}, {"FC_FLAT_UNROLL": "2"}, {"FC_FLAT_UNROLL": "4"},  # every FLAT unroll build
-    {"FC_EXIT": "rank"}, {"FC_EXIT": "cta"},            # both exit protocols (coll_common.cuh)
+    {"FC_EXIT": "push"}, {"FC_EXIT": "cta"},            # the other exit protocols (coll_common.cuh)
     {"FC_FLAT_MAP": "stride"},                          # the plain grid-stride FLAT work mapping
 ])
 def test_every_kernel_build_bitexact(knobs):

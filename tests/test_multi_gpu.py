@@ -30,7 +30,7 @@ def test_real_world_parity(nproc):
 
 
 @pytest.mark.parametrize("nproc", [2, 4])
-@pytest.mark.parametrize("exit_mode", ["cta", "rank"])
+@pytest.mark.parametrize("exit_mode", ["cta", "push"])
 def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
     """The same worker with the size-dependent kernel choices forced the other
     way: tree kernels with the 2-CTA/SM register budget, FLAT with unroll 1 and
@@ -43,6 +43,27 @@ def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
                FC_HOST_STAGES="3", FC_MP_STRESS="1500")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={29610 + nproc}", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    for k in range(nproc):
+        assert f"MP_OK {k}" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("nproc,exit_mode", [(2, "poll"), (2, "push"), (2, "cta"), (4, "poll")])
+def test_real_world_on_one_gpu(nproc, exit_mode):
+    """The real multi-process path -- CUDA-IPC heaps, one process per rank, the
+    cross-process entry/exit stamp protocol (c.rank >= 0), every schedule, op,
+    host path and the random back-to-back stress, bit-exact vs the oracle --
+    on a ONE-GPU box: the ranks share GPU 0 (gloo bootstrap; their kernels
+    time-slice, so this checks values and the protocol, not speed)."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, FC_MP_GPUS="1", FC_MP_SIZES="5,16391,300007", FC_MP_STRESS="40", FC_MP_TIMEOUT="30",
+               FC_MP_TIMEOUT_TEST="0", OMP_NUM_THREADS="1", FC_EXIT=exit_mode)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={29640 + 4 * nproc + ('poll', 'push', 'cta').index(exit_mode)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]

@@ -339,8 +339,39 @@ def test_lr_schedules_spec_and_paper_values():
     assert abs(oracle.lr_at("multistep", 0.01, 250_000, **st) - 0.0001) <= float(_ulp(0.0001))
     assert oracle.lr_at("step", 0.04, 25, gamma=0.5, stepsize=10) == np.float32(0.01)
     assert oracle.lr_at("fixed", 0.08, 123) == np.float32(0.08)
-    with pytest.raises(ValueError):
-        oracle.lr_at("poly", 0.01, 1001, max_iter=1000)
+    # past max_iter the schedule stays at its end value (reading R21): (1 - 1)^0.5 = 0
+    assert oracle.lr_at("poly", 0.01, 1001, max_iter=1000) == 0.0
+    assert oracle.lr_at("poly", 0.01, 10**9, max_iter=1000) == 0.0
+    assert oracle.lr_at("poly", 0.01, 5000, power=0.0, max_iter=1000) == np.float32(0.01)  # 0^0 = 1
+    for bad in (dict(power=-0.5, max_iter=10), dict(power=float("inf"), max_iter=10)):
+        with pytest.raises(ValueError):
+            oracle.lr_at("poly", 0.01, 3, **bad)
+    for g in (0.0, -0.1, float("nan")):
+        with pytest.raises(ValueError):
+            oracle.lr_at("step", 0.01, 3, gamma=g, stepsize=2)
+        with pytest.raises(ValueError):
+            oracle.lr_at("multistep", 0.01, 3, gamma=g, steps=(1,))
     # poly is non-increasing (SPEC invariant)
     vals = [oracle.lr_at("poly", 0.08, i, max_iter=97) for i in range(98)]
     assert all(a >= b for a, b in zip(vals, vals[1:]))
+
+
+def test_openmp_build_is_the_same_oracle():
+    """The OpenMP build (bench.py's all-cores CPU baseline) splits elements
+    over threads without touching any element's arithmetic: identical bits to
+    the single-threaded oracle for the tree sum, the PS-order tree and SGD."""
+    import os
+    rng = np.random.default_rng(7)
+    t = oracle.omp_threads(max(2, min(8, os.cpu_count() or 2)))
+    assert t >= 2
+    for p, n in ((1, 17), (4, 100_003), (8, 65_537), (5, 4096 + 3)):
+        g = (rng.standard_normal((p, n)) * 10.0 ** rng.uniform(-5, -1, (p, 1))).astype(np.float32)
+        for k in (2, 3, p + 1):
+            a, b = oracle.tree_sum(g, k), oracle.tree_sum(g, k, omp=True)
+            np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+        w = rng.standard_normal(n).astype(np.float32) * 0.01
+        v = rng.standard_normal(n).astype(np.float32) * 1e-4
+        w1, v1 = oracle.fused_step(g, w, v, 0.04, 0.9, 5e-4, 1024)
+        w2, v2 = oracle.fused_step(g, w, v, 0.04, 0.9, 5e-4, 1024, omp=True)
+        np.testing.assert_array_equal(w1.view(np.uint32), w2.view(np.uint32))
+        np.testing.assert_array_equal(v1.view(np.uint32), v2.view(np.uint32))
