@@ -131,29 +131,34 @@ static float inv_batch(int64_t batch) {
 }
 
 // Exit protocol of the collectives (coll_common.cuh exit_rank): rank-level,
-// the last CTA per GPU does one sys fence and writes its stamp into its own
-// heap, peers poll it over NVLink (default, FC_EXIT=poll); the same with the
-// stamps pushed into the peers' heaps (FC_EXIT=push, round 1's default); or,
-// with FC_EXIT=cta, the per-CTA exit barrier.  Measured in
-// profiles/r01_sweep_exit_* (cta vs push) and profiles/r02_* (push vs poll).
+// the last CTA per GPU does one sys fence and pushes its stamp into every
+// peer's heap (default, FC_EXIT=push); the same with the stamp written into
+// its own heap and polled by the peers over NVLink (FC_EXIT=poll: measured
+// equal, profiles/r02_exit_push_vs_poll.txt); or, with FC_EXIT=cta, the
+// per-CTA exit barrier (profiles/r01_sweep_exit_*).
 // Part of the call signature, so ranks that disagree fail with FC_ERR_MISMATCH
 // at entry instead of waiting on stamps that never come.
 static int exit_mode() {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("FC_EXIT");
-        m = (e && strcmp(e, "cta") == 0) ? 0 : (e && (strcmp(e, "push") == 0 || strcmp(e, "rank") == 0)) ? 1 : 2;
+        m = (e && strcmp(e, "cta") == 0) ? 0 : (e && strcmp(e, "poll") == 0) ? 2 : 1;
     }
     return m;
 }
 
-// FLAT work mapping (coll_flat.cuh): balanced slab rows by default;
-// FC_FLAT_MAP=stride selects the plain grid stride (A/B experiments).  Value-neutral.
-static int flat_map_stride() {
+// FLAT work mapping (coll_flat.cuh): dynamic guided claims from a per-rank
+// counter (default, FC_FLAT_MAP=dyn; push broadcast only, the pull path pairs
+// elements statically and uses the balanced rows), balanced static slab rows
+// (balanced, round 1's default) or the plain grid stride (stride).  Measured
+// (profiles/r02_flat_map_p2.txt): dyn 0.9-2.2 % faster than balanced at
+// p = 2 from NiN to AlexNet size.  Value-neutral (every element is processed
+// once, same arithmetic), so not part of the call signature.
+static int flat_map() {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("FC_FLAT_MAP");
-        m = (e && strcmp(e, "stride") == 0) ? 1 : 0;
+        m = (e && strcmp(e, "stride") == 0) ? 1 : (e && strcmp(e, "balanced") == 0) ? 0 : 2;
     }
     return m;
 }
@@ -229,8 +234,8 @@ static fc_status world_common(fc_world* w, int world_size, int dev, int64_t heap
     if (w->layout.total_bytes >= heap_bytes) return FC_ERR_INVALID_ARG;
     if (cudaMalloc(&w->d_status, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
     if (cudaMemset(w->d_status, 0, sizeof(int)) != cudaSuccess) return FC_ERR_CUDA;
-    if (cudaMalloc(&w->d_ctl, 2 * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
-    if (cudaMemset(w->d_ctl, 0, 2 * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMalloc(&w->d_ctl, FC_CTL_WORDS * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
+    if (cudaMemset(w->d_ctl, 0, FC_CTL_WORDS * sizeof(uint32_t)) != cudaSuccess) return FC_ERR_CUDA;
     default_config(w);
     return FC_OK;
 }
@@ -531,7 +536,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.rank_exit = exit_mode();
     c.win_k = win_k;
     c.win_s = win_s;
-    c.map_stride = flat_map_stride();
+    c.flat_map = flat_map();
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;

@@ -97,6 +97,7 @@ __device__ __forceinline__ void epoch_end(const FcColl& c) {
         const uint32_t done = atomicAdd(c.ctl + 1, 1u) + 1u;
         if (done == total) {
             c.ctl[1] = 0u;
+            for (int r = 0; r < FC_MAX_RANKS; ++r) c.ctl[FC_CTL_CLAIM + r] = 0u;
             advance_lr(c);
             __threadfence();
             atomicExch(c.ctl, s_epoch);
@@ -168,14 +169,13 @@ static __device__ bool cta_barrier(const FcColl& c, int rank, int slot) {
 // increment -> last CTA's increment + fence.gpu (same GPU) -> fence.sys +
 // stamp -> the peer's acquire.sys of the stamp.  The other CTAs leave at once.
 // Where the stamp goes:
-//   1 (push): into every peer's heap; each rank polls its own heap (local
-//     loads).  The stamps are remote stores issued after the fence, and a
-//     kernel that ends with remote stores in flight waits ~4 us longer to
-//     complete (scripts/gap_bench.cu: 9.7 vs 5.8 us).
-//   2 (poll, default): into the rank's OWN heap; the last CTA's threads q < p
-//     poll peer q's stamp word over NVLink with acquire loads, in parallel.
-//     No remote store follows the fence, so the kernel completes like one
-//     that only wrote locally.
+//   1 (push, default): into every peer's heap; each rank polls its own heap
+//     (local loads).
+//   2 (poll): into the rank's OWN heap; the last CTA's threads q < p poll
+//     peer q's stamp word over NVLink with acquire loads, in parallel, so no
+//     remote store follows the fence.  Measured the same as push at p = 2
+//     (profiles/r02_exit_push_vs_poll.txt): the stamps are not what makes
+//     the kernel's completion slower than an empty kernel's.
 // Then the epoch advances as in epoch_end.  Virtual worlds: the last CTA of
 // the whole grid already follows every rank's CTAs, no stamps needed.
 // `cta_slot`: which slot-1 stamp word carries the exit (0; the FLAT pull path,
@@ -229,6 +229,7 @@ static __device__ __forceinline__ void exit_rank(const FcColl& c, int rank, int 
     }
     if (t == 0) {
         c.ctl[1] = 0u;
+        for (int r = 0; r < FC_MAX_RANKS; ++r) c.ctl[FC_CTL_CLAIM + r] = 0u;
         advance_lr(c);
         __threadfence();
         atomicExch(c.ctl, s_epoch);

@@ -16,7 +16,7 @@ namespace fc {
 // produced by the peer CTA with this CTA's index — the per-CTA barrier only
 // orders that CTA's writes, so this must enumerate exactly the element set the
 // data phase gives CTA blockIdx.x (balanced: me + s*G*T for every slab s;
-// c.map_stride: the plain grid stride).
+// c.flat_map == 1: the plain grid stride; the pull path never uses the dynamic map).
 template <int P, int U>
 __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
     const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
@@ -38,8 +38,8 @@ __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
     float4* dst = reinterpret_cast<float4*>(fused ? w_of(c, rank) : grad_of(c, rank));
     const int64_t T = FLAT_T;
     const int64_t GT = (int64_t)gridDim.x * T;
-    const int64_t me = c.map_stride ? (int64_t)blockIdx.x * T * U + threadIdx.x : (int64_t)blockIdx.x * T + threadIdx.x;
-    const int64_t step = c.map_stride ? T : GT;  // between this thread's U elements of one pass
+    const int64_t me = c.flat_map == 1 ? (int64_t)blockIdx.x * T * U + threadIdx.x : (int64_t)blockIdx.x * T + threadIdx.x;
+    const int64_t step = c.flat_map == 1 ? T : GT;  // between this thread's U elements of one pass
     for (int64_t rel = me; rel < maxlen; rel += GT * U) {
         float4 x[U][P];
 #pragma unroll
@@ -70,10 +70,85 @@ __device__ __forceinline__ void pull_results(const FcColl& c, int rank) {
     }
 }
 
+// One "row" of the FLAT data phase for this thread: elements rb + j*step for
+// j < nv (and < ce), U float4 per rank in flight.  Loads the P ranks' values,
+// evaluates the K-nomial tree in registers (R1), then (fused) applies SGD and
+// stores v' locally and w' to every rank (pull: only locally), or (allreduce /
+// PS) stores the sum to every rank's grad (pull: only locally).
+template <int P, int K, int U>
+__device__ __forceinline__ void flat_row(const FcColl& c, int rank, int64_t rb, int nv, int64_t step,
+                                         int64_t ce, bool fused, bool pull) {
+#define FC_IX(j) ((j) < nv ? rb + (int64_t)(j) * step : ce)
+    float4 x[U][P];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+        const int64_t i = FC_IX(j);
+        if (i < ce) {
+#pragma unroll
+            for (int q = 0; q < P; ++q) x[j][q] = ld_cg(reinterpret_cast<const float4*>(grad_of(c, q)) + i);
+        }
+    }
+    if (fused) {
+        float4 w[U], v[U];
+        float4* w4 = reinterpret_cast<float4*>(w_of(c, rank));
+        float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = FC_IX(j);
+            if (i < ce) {
+                w[j] = ld_rw(w4 + i);
+                v[j] = ld_rw(v4 + i);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = FC_IX(j);
+            if (i < ce) {
+                const float4 S = tree_sum_regs<P, K>(x[j]);
+                sgd4_any(c.segs, 4 * i, S, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
+                st_na(v4 + i, v[j]);
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (!pull || q == rank) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+            const int64_t i = FC_IX(j);
+            if (i < ce) {
+                const float4 S = tree_sum_regs<P, K>(x[j]);
+#pragma unroll
+                for (int q = 0; q < P; ++q)
+                    if (!pull || q == rank) st_na(reinterpret_cast<float4*>(grad_of(c, q)) + i, S);
+            }
+        }
+    }
+#undef FC_IX
+}
+
+// Dynamic work claims (c.flat_map == 2, push broadcast): the slice is cut into
+// units of T consecutive float4 (one per thread, coalesced); CTAs claim runs
+// of g <= U consecutive units from a per-rank counter (ctl[FC_CTL_CLAIM +
+// rank], zeroed again by the call's last CTA), g shrinking towards 1 as the
+// slice runs out (guided: about remaining / 2G units per claim), so the CTAs
+// that the NVLink/switch serves faster take more work and all of them finish
+// within about one unit's time of each other.  Thread 0 issues the next claim
+// right after the current row's loads are in flight, so its latency hides
+// behind the row.  All CTAs still sweep the slice front to back together.
+__shared__ int64_t s_claim[2];
+__shared__ int s_claim_n[2];
+__device__ __forceinline__ int guided_units(int64_t total, int64_t next, int G, int U) {
+    const int64_t rem = total - next;
+    int64_t g = rem / (2 * (int64_t)G);
+    return (int)(g < 1 ? 1 : g > U ? U : g);
+}
+
 template <int P, int K, int U>
 __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ FcColl c) {
     const int rank = my_rank(c);
     const bool pull = c.bcast == FC_BCAST_PULL && c.op != FC_OP_PS;
+    const bool dyn = c.flat_map == 2 && !pull;  // pull pairs elements with the peer CTA's: static only
     epoch_begin(c);
     trace(c, 0);
     const bool ok = cta_barrier(c, rank, 0);
@@ -96,77 +171,67 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
             int64_t i0 = e0 / 4, ce = i1;
             if (c.win_s > 1) window_range(e0 / 4, i1, c.win_k, c.win_s, &i0, &ce);
             const bool tail_here = c.win_s <= 1 || c.win_k == c.win_s - 1;
-            // Work mapping.  A "slab" is G*T consecutive float4s (one per thread of the
-            // grid, coalesced); the slice is nslab slabs.  Default (balanced): rows of
-            // <= U slabs, the slabs spread evenly over ceil(nslab / U) rows, so every
-            // CTA does the same work in every row and all CTAs finish together.
-            // c.map_stride (FC_FLAT_MAP=stride): the plain grid stride, where the last
-            // partial row of G*T*U belongs to the first CTAs and the others idle.
+            const int64_t GT = (int64_t)gridDim.x * T;
+            const int64_t M = ce - i0;
+            // Static work mapping.  A "slab" is G*T consecutive float4s (one per
+            // thread of the grid, coalesced); the slice is nslab slabs.  Default
+            // (balanced): rows of <= U slabs, the slabs spread evenly over
+            // ceil(nslab / U) rows, so every CTA does the same work in every row.
+            // c.flat_map == 1 (FC_FLAT_MAP=stride): the plain grid stride, where the
+            // last partial row of G*T*U belongs to the first CTAs and the others idle.
             // Either way all CTAs sweep the slice in lockstep, so at any moment the
             // GPU's remote reads fall in one few-MB window of each peer's heap (a
             // contiguous range per CTA measured ~10% slower: 444 scattered streams).
-            const int64_t GT = (int64_t)gridDim.x * T;
-            const int64_t M = ce - i0;
+            // Dynamic (dyn): rows are the claimed runs of units (above).
+            const bool stride = c.flat_map == 1;
             const int64_t nslab = (M + GT - 1) / GT;
-            const int64_t rows = c.map_stride ? (M + GT * U - 1) / (GT * U) : (nslab + U - 1) / U;
-            const int64_t me = c.map_stride ? (int64_t)blockIdx.x * T * U + threadIdx.x
-                                            : (int64_t)blockIdx.x * T + threadIdx.x;
-            const int64_t step = c.map_stride ? T : GT;
-            int64_t s0 = 0;
-            for (int64_t r = 0; r < rows; ++r) {
-                // element j of this thread in row r: rb + j * step, for j < nv (and < ce)
-                const int64_t s1 = c.map_stride ? 0 : nslab * (r + 1) / rows;
-                const int64_t rb = c.map_stride ? i0 + r * GT * U + me : i0 + s0 * GT + me;
-                const int nv = c.map_stride ? U : (int)(s1 - s0);
-                s0 = s1;
-#define FC_IX(j) ((j) < nv ? rb + (int64_t)(j) * step : ce)
-                float4 x[U][P];
-#pragma unroll
-                for (int j = 0; j < U; ++j) {
-                    const int64_t i = FC_IX(j);
-                    if (i < ce) {
-#pragma unroll
-                        for (int q = 0; q < P; ++q)
-                            x[j][q] = ld_cg(reinterpret_cast<const float4*>(grad_of(c, q)) + i);
-                    }
+            const int64_t rows = stride ? (M + GT * U - 1) / (GT * U) : (nslab + U - 1) / U;
+            const int64_t me = stride ? (int64_t)blockIdx.x * T * U + threadIdx.x
+                                      : (int64_t)blockIdx.x * T + threadIdx.x;
+            const int64_t total = (M + T - 1) / T;  // dyn: units of T float4
+            const int G = gridDim.x;
+            uint32_t* ctr = c.ctl + FC_CTL_CLAIM + rank;
+            if (dyn) {
+                if (threadIdx.x == 0) {
+                    const int g = guided_units(total, 0, G, U);
+                    s_claim[0] = (int64_t)atomicAdd(ctr, (uint32_t)g);
+                    s_claim_n[0] = g;
                 }
-                if (fused) {
-                    float4 w[U], v[U];
-                    float4* w4 = reinterpret_cast<float4*>(w_of(c, rank));
-                    float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const int64_t i = FC_IX(j);
-                        if (i < ce) {
-                            w[j] = ld_rw(w4 + i);
-                            v[j] = ld_rw(v4 + i);
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const int64_t i = FC_IX(j);
-                        if (i < ce) {
-                            const float4 S = tree_sum_regs<P, K>(x[j]);
-                            sgd4_any(c.segs, 4 * i, S, w[j], v[j], s_lr, c.mu, c.wd, c.inv_b);
-                            st_na(v4 + i, v[j]);
-#pragma unroll
-                            for (int q = 0; q < P; ++q)
-                                if (!pull || q == rank) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
-                        }
+                __syncthreads();
+            }
+            int64_t s0 = 0;
+            for (int64_t r = 0;; ++r) {
+                // element j of this thread in row r: rb + j * step, for j < nv (and < ce)
+                int64_t rb, step;
+                int nv;
+                uint32_t next = 0;
+                int gnext = 0;
+                if (dyn) {
+                    const int64_t u0 = s_claim[r & 1];
+                    if (u0 >= total) break;
+                    nv = (int)min((int64_t)s_claim_n[r & 1], total - u0);
+                    rb = i0 + u0 * T + threadIdx.x;
+                    step = T;
+                    if (threadIdx.x == 0) {  // the next claim; its result is needed only after this row
+                        gnext = guided_units(total, u0 + nv, G, U);
+                        next = atomicAdd(ctr, (uint32_t)gnext);
                     }
                 } else {
-#pragma unroll
-                    for (int j = 0; j < U; ++j) {
-                        const int64_t i = FC_IX(j);
-                        if (i < ce) {
-                            const float4 S = tree_sum_regs<P, K>(x[j]);
-#pragma unroll
-                            for (int q = 0; q < P; ++q)
-                                if (!pull || q == rank) st_na(reinterpret_cast<float4*>(grad_of(c, q)) + i, S);
-                        }
-                    }
+                    if (r >= rows) break;
+                    const int64_t s1 = stride ? 0 : nslab * (r + 1) / rows;
+                    rb = stride ? i0 + r * GT * U + me : i0 + s0 * GT + me;
+                    nv = stride ? U : (int)(s1 - s0);
+                    step = stride ? T : GT;
+                    s0 = s1;
                 }
-#undef FC_IX
+                flat_row<P, K, U>(c, rank, rb, nv, step, ce, fused, pull);
+                if (dyn) {
+                    if (threadIdx.x == 0) {
+                        s_claim[(r + 1) & 1] = (int64_t)next;
+                        s_claim_n[(r + 1) & 1] = gnext;
+                    }
+                    __syncthreads();
+                }
             }
             // trailing n % 4 elements of the last slice
             const int rem = (int)(e1 - 4 * i1);

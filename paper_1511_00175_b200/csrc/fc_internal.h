@@ -113,10 +113,15 @@ struct FcColl {
     uint64_t* trace;   // optional: per-CTA %globaltimer stamps [rank][cta][FC_TRACE_SLOTS]
     int rank_exit;     // 1: rank-level exit (one sys fence per GPU), 0: per-CTA exit barrier
     int win_k, win_s;  // FLAT push only: process window win_k of win_s of the owned slice (win_s <= 1: all)
-    int map_stride;    // FLAT: 1 = plain grid-stride work mapping, 0 = balanced slab rows (default)
+    int flat_map;      // FLAT work mapping: 0 = balanced slab rows, 1 = plain grid stride, 2 = dynamic claims
 };
 
-#define FC_TRACE_SLOTS 4  // kernel entry, after entry barrier, after the data phase, exit
+#define FC_TRACE_SLOTS 4
+// device call-control words (fc_world::d_ctl): [0] epoch of the last completed call,
+// [1] CTAs finished in the current call, [FC_CTL_CLAIM + r] rank r's FLAT work-claim
+// counter (dynamic mapping); the call's last CTA zeroes [1] and the claim counters
+#define FC_CTL_CLAIM 2
+#define FC_CTL_WORDS (FC_CTL_CLAIM + FC_MAX_RANKS)  // kernel entry, after entry barrier, after the data phase, exit
 
 enum FcOp {
     FC_OP_ALLREDUCE = 0,

@@ -76,6 +76,41 @@ __global__ void store_kernel(float4* dst, int per, int fence, uint64_t* span) {
     }
 }
 
+// The collectives' rank-level exit, step by step (coll_common.cuh exit_rank):
+// every CTA stores `per` float4 per thread (remote or local), orders them with
+// a gpu fence (or a sys fence: bit 8) and arrives on a counter; the last CTA
+// then does: bit 1 fence.sys, bit 2 a remote relaxed stamp store, bit 4 a
+// remote acquire load, bit 16 a LOCAL relaxed stamp store, then resets the
+// counter and bumps the epoch.  Which step makes the kernel's completion slow?
+__global__ void proto_kernel(float4* dst, int per, int mode, uint32_t* ctl, uint64_t* rflag,
+                             uint64_t* lflag, uint64_t* span) {
+    const uint64_t t0 = gt();
+    const float4 v = make_float4(1, 2, 3, 4);
+    for (int j = 0; j < per; ++j) dst[((int64_t)blockIdx.x * per + j) * blockDim.x + threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (mode & 8) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else __threadfence();
+        const uint32_t done = atomicAdd(ctl + 1, 1u) + 1u;
+        if (done == gridDim.x) {
+            __threadfence();
+            if (mode & 1) asm volatile("fence.acq_rel.sys;" ::: "memory");
+            if (mode & 2) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(rflag), "l"((uint64_t)t0) : "memory");
+            if (mode & 16) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(lflag), "l"((uint64_t)t0) : "memory");
+            if (mode & 4) {
+                uint64_t x;
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(rflag) : "memory");
+                if (x == 1) ctl[3] = 1;
+            }
+            ctl[1] = 0u;
+            __threadfence();
+            atomicExch(ctl, ctl[0] + 1);
+        }
+        span[2 * blockIdx.x] = t0;
+        span[2 * blockIdx.x + 1] = gt();
+    }
+}
+
 int main() {
     int ndev = 0;
     cudaGetDeviceCount(&ndev);
@@ -111,6 +146,11 @@ int main() {
                 case 2: big_kernel<<<G, T, 0, st>>>(big, span); break;
                 case 3: counter_kernel<<<G, T, 0, st>>>(ctl, span); break;
                 case 4: store_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, span); break;
+                case 5:
+                    proto_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, ctl,
+                                                  (uint64_t*)(remote ? peer : local) + (5 << 20),
+                                                  (uint64_t*)local + (6 << 20), span);
+                    break;
             }
             cudaEventRecord(e1, st);
             cudaEventSynchronize(e1);
@@ -148,6 +188,15 @@ int main() {
         run("remote stores x1 + fence.sys", 148, 512, 4, 1, 1, true);
         run("remote stores x16", 148, 512, 4, 16, 0, true);
         run("remote stores x16 + fence.sys", 148, 512, 4, 16, 1, true);
+        run("exit: remote x4, gpu fence + ctr", 148, 512, 5, 4, 0, true);
+        run("exit: + last fence.sys", 148, 512, 5, 4, 1, true);
+        run("exit: + last fence.sys + rstamp", 148, 512, 5, 4, 3, true);
+        run("exit: + last fence.sys + racq", 148, 512, 5, 4, 5, true);
+        run("exit: + last fence.sys + lstamp", 148, 512, 5, 4, 17, true);
+        run("exit: all sys fence + ctr", 148, 512, 5, 4, 8, true);
+        run("exit: all sys + last rstamp", 148, 512, 5, 4, 10, true);
+        run("exit: local x4, gpu fence + ctr", 148, 512, 5, 4, 0, false);
+        run("exit: local + last fence.sys", 148, 512, 5, 4, 1, false);
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
