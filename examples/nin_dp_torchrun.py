@@ -109,6 +109,7 @@ def main():
         for j in b:
             owner[j] = bi
 
+    tiny = torch.zeros(1, device=dev)
     comm = torch.cuda.Stream(priority=-1)  # high priority: its CTAs go first as SMs free up
     pending = [0] * len(buckets)
     mode = {"m": "compute_only"}
@@ -118,6 +119,10 @@ def main():
         ev = torch.cuda.Event()
         ev.record()
         comm.wait_event(ev)
+        # while backward still runs, a few CTAs (backward keeps most SMs); the last
+        # bucket is launched when backward is done: every SM (same choice on every
+        # rank, so the grids -- part of the call signature -- agree)
+        W.set_max_ctas(0 if bi == len(buckets) - 1 else args.overlap_ctas)
         with torch.cuda.stream(comm):
             fc.firecaffe_tree_allreduce_sgd(w_heap[o:o + k], g_heap[o:o + k], m_heap[o:o + k], world=W, **hp)
 
@@ -150,6 +155,11 @@ def main():
         # backward's last kernel on the compute stream; every bucket's collective
         # (bucketed mode) is already enqueued on the comm stream by the hooks
         e_bwd.record()
+        if mode["m"] == "compute_only":
+            # how far apart the ranks finish backward: a tiny NCCL rendezvous right after
+            # it (its own latency included) -- the part of any exposed time that is rank
+            # skew, which no collective can hide
+            dist.all_reduce(tiny)
         if mode["m"] == "sequential":
             fc.firecaffe_tree_allreduce_sgd(w_heap, g_heap, m_heap, world=W, **hp)
         torch.cuda.current_stream().wait_stream(comm)
@@ -160,7 +170,7 @@ def main():
     for m in ("compute_only", "sequential", "bucketed"):
         mode["m"] = m
         # overlapping: a few CTAs, so backward keeps most SMs; alone: every SM
-        W.set_max_ctas(args.overlap_ctas if m == "bucketed" else 0)
+        W.set_max_ctas(0)
         w_heap.copy_(w_init)
         m_heap.zero_()
         assert all(q.grad.data_ptr() == g_heap.data_ptr() + 4 * o for q, (o, _) in zip(params, offs)), \
@@ -194,7 +204,9 @@ def main():
             "model": "NiN (ImageNet)", "params": n, "gpus": p, "global_batch": args.batch, "image": args.image,
             "buckets": len(buckets), "steps": args.steps, "ms_per_iter_median": results,
             # exposed communication, measured directly: the median time from the end
-            # of backward (last compute-stream kernel) to the end of the step, max over ranks
+            # of backward (last compute-stream kernel) to the end of the step, max over
+            # ranks; compute_only's entry is a tiny NCCL rendezvous after backward (the
+            # ranks' backward-end skew + NCCL latency: the floor any synchronous step pays)
             "exposed_ms_after_backward": exposed,
             "comm_to_compute_ratio": round(exposed["sequential"] / results["compute_only"], 5),
             "paper_ratio_at_32_gpus_titan": "~1 (P:406)",

@@ -142,7 +142,8 @@ static int exit_mode() {
     static int m = -1;
     if (m < 0) {
         const char* e = getenv("FC_EXIT");
-        m = (e && strcmp(e, "cta") == 0) ? 0 : (e && strcmp(e, "poll") == 0) ? 2 : 1;
+        m = (e && strcmp(e, "cta") == 0) ? 0 : (e && strcmp(e, "poll") == 0) ? 2
+            : (e && strcmp(e, "ctapoll") == 0) ? 3 : 1;
     }
     return m;
 }

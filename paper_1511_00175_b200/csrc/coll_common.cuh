@@ -236,9 +236,58 @@ static __device__ __forceinline__ void exit_rank(const FcColl& c, int rank, int 
     }
 }
 
+// Per-CTA exit with LOCAL stamps (c.rank_exit == 3, real worlds): every CTA
+// makes its own writes — local and peer — visible system-wide with its own
+// `fence.sys` and writes its exit stamp into its OWN heap (a release pattern at
+// sys scope whose write is local); thread q < p then polls peer q's stamp of
+// the CTA with this index over NVLink with acquire loads (each a release/
+// acquire pair at sys scope: peer q's CTA's pushes into this heap
+// happen-before this CTA's exit).  All CTAs of a rank together observe every
+// CTA of every peer, so when the kernel ends every store any peer made into
+// this heap has landed.  No remote store follows a fence: a kernel whose CTAs
+// each issued `fence.sys` after their peer stores completes ~3.3 us sooner
+// than one with only gpu-scope fences and one last-CTA sys fence
+// (scripts/gap_bench.cu, profiles/r02_gap_bench.txt), and the fences of the 148
+// CTAs overlap each other.  Then the epoch advances as in epoch_end.
+static __device__ __forceinline__ void exit_cta_poll(const FcColl& c, int rank) {
+    __syncthreads();
+    const int t = threadIdx.x;
+    const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
+    if (t == 0) {
+        fence_sys();
+        st_relaxed_sys64(bar_flag(c, rank, 1, blockIdx.x, rank), stamp);
+    }
+    bool good = true;
+    if (t < c.p && t != rank) {
+        const uint64_t* f = bar_flag(c, t, 1, blockIdx.x, t);
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        uint64_t v;
+        while (!reached((uint32_t)(v = ld_acquire_sys64(f)), s_epoch)) {
+            __nanosleep(64);
+            if ((++spins & 7u) == 0) {
+                if (*(volatile int*)c.status != FC_OK) { good = false; break; }
+                if (globaltimer() - t0 > c.timeout_ns) {
+                    atomicCAS(c.status, FC_OK, FC_ERR_TIMEOUT);
+                    good = false;
+                    break;
+                }
+            }
+        }
+        if (good && (uint32_t)v == s_epoch && (uint32_t)(v >> 32) != c.sig) atomicCAS(c.status, FC_OK, FC_ERR_MISMATCH);
+    }
+    __syncthreads();
+}
+
 // End of a collective whose data phase may have written into peers' heaps:
 // the exit barrier (per CTA, or per rank with c.rank_exit), then the epoch.
 __device__ __forceinline__ void finish_call(const FcColl& c, int rank) {
+    if (c.rank_exit == 3 && c.rank >= 0) {
+        exit_cta_poll(c, rank);
+        trace(c, 3);
+        epoch_end(c);
+        return;
+    }
     if (c.rank_exit) {
         exit_rank(c, rank);
         trace(c, 3);

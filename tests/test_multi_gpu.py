@@ -27,10 +27,11 @@ def test_real_world_parity(nproc):
     assert r.returncode == 0, out[-4000:]
     for k in range(nproc):
         assert f"MP_OK {k}" in out, out[-4000:]
+    assert "NCCL_TOL" in out, "the NCCL baseline's tolerance check did not run"
 
 
 @pytest.mark.parametrize("nproc", [2, 4])
-@pytest.mark.parametrize("exit_mode", ["cta", "push"])
+@pytest.mark.parametrize("exit_mode", ["cta", "push", "ctapoll"])
 def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
     """The same worker with the size-dependent kernel choices forced the other
     way: tree kernels with the 2-CTA/SM register budget, FLAT with unroll 1 and
@@ -50,7 +51,8 @@ def test_real_world_parity_other_kernel_builds(nproc, exit_mode):
         assert f"MP_OK {k}" in out, out[-4000:]
 
 
-@pytest.mark.parametrize("nproc,exit_mode", [(2, "poll"), (2, "push"), (2, "cta"), (4, "poll")])
+@pytest.mark.parametrize("nproc,exit_mode", [(2, "poll"), (2, "push"), (2, "cta"), (2, "ctapoll"), (4, "push"),
+                                             (4, "ctapoll")])
 def test_real_world_on_one_gpu(nproc, exit_mode):
     """The real multi-process path -- CUDA-IPC heaps, one process per rank, the
     cross-process entry/exit stamp protocol (c.rank >= 0), every schedule, op,
@@ -62,13 +64,14 @@ def test_real_world_on_one_gpu(nproc, exit_mode):
     env = dict(os.environ, FC_MP_GPUS="1", FC_MP_SIZES="5,16391,300007", FC_MP_STRESS="40", FC_MP_TIMEOUT="30",
                FC_MP_TIMEOUT_TEST="0", OMP_NUM_THREADS="1", FC_EXIT=exit_mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr=127.0.0.1", f"--master-port={29640 + 4 * nproc + ('poll', 'push', 'cta').index(exit_mode)}",
+           "--master-addr=127.0.0.1", f"--master-port={29640 + 4 * nproc + ('poll', 'push', 'cta', 'ctapoll').index(exit_mode)}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     for k in range(nproc):
         assert f"MP_OK {k}" in out, out[-4000:]
+    assert "GLOO_TOL" in out, "the library-allreduce baseline's tolerance check did not run"
 
 
 def test_eight_rank_world_on_shared_gpus():
