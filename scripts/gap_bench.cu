@@ -111,6 +111,25 @@ __global__ void proto_kernel(float4* dst, int per, int mode, uint32_t* ctl, uint
     }
 }
 
+// remote (or local) 128-bit loads, summed so they cannot be dropped, optional fence.sys
+__global__ void load_kernel(const float4* src, int per, int fence, uint64_t* span, float* sink) {
+    const uint64_t t0 = gt();
+    float acc = 0.f;
+    for (int j = 0; j < per; ++j) {
+        float4 v;
+        const float4* p = src + ((int64_t)blockIdx.x * per + j) * blockDim.x + threadIdx.x;
+        asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        acc += v.x + v.y + v.z + v.w;
+    }
+    if (acc == 12345.f) sink[0] = acc;
+    if (fence) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        span[2 * blockIdx.x] = t0;
+        span[2 * blockIdx.x + 1] = gt();
+    }
+}
+
 int main() {
     int ndev = 0;
     cudaGetDeviceCount(&ndev);
@@ -146,6 +165,7 @@ int main() {
                 case 2: big_kernel<<<G, T, 0, st>>>(big, span); break;
                 case 3: counter_kernel<<<G, T, 0, st>>>(ctl, span); break;
                 case 4: store_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, span); break;
+                case 6: load_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, span, (float*)local); break;
                 case 5:
                     proto_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, ctl,
                                                   (uint64_t*)(remote ? peer : local) + (5 << 20),
@@ -197,6 +217,10 @@ int main() {
         run("exit: all sys + last rstamp", 148, 512, 5, 4, 10, true);
         run("exit: local x4, gpu fence + ctr", 148, 512, 5, 4, 0, false);
         run("exit: local + last fence.sys", 148, 512, 5, 4, 1, false);
+        run("remote loads x4", 148, 512, 6, 4, 0, true);
+        run("remote loads x16", 148, 512, 6, 16, 0, true);
+        run("remote loads x16 + fence.sys", 148, 512, 6, 16, 1, true);
+        run("local loads x16", 148, 512, 6, 16, 0, false);
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
