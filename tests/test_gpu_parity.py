@@ -995,3 +995,71 @@ def test_every_kernel_build_bitexact(knobs):
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu", "-k", sel,
                         "-p", "no:cacheprovider"], env=env, cwd=ROOT, capture_output=True, text=True, timeout=1800)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+# ------------------------------------------- beyond 2^31 elements (64-bit indexing) --
+BIG_N = (1 << 31) + 4099  # > INT32_MAX floats per buffer; buffers at heap offsets > 2^34 bytes
+
+
+def _big_enough(gb):
+    free, _ = torch.cuda.mem_get_info()
+    return free > gb * (1 << 30)
+
+
+def test_sgd_step_beyond_2_31_elements():
+    """The 1-GPU SGD at n > 2^31 (8.6 GB per vector): 64-bit element indexing
+    everywhere, checked bit-exactly against the oracle on sampled indices
+    spread over the whole range, including the last ragged float4."""
+    if not _big_enough(30):
+        pytest.skip("needs ~30 GB of free device memory")
+    n = BIG_N
+    g = torch.randn(n, device="cuda") * 1e-2
+    w = torch.randn(n, device="cuda") * 1e-2
+    v = torch.randn(n, device="cuda") * 1e-4
+    gen = torch.Generator().manual_seed(31)
+    idx = torch.cat([torch.randint(0, n, (20000,), generator=gen), torch.arange(n - 9, n),
+                     torch.arange((1 << 31) - 5, (1 << 31) + 5)]).cuda()
+    g0, w0, v0 = g[idx].cpu().numpy(), w[idx].cpu().numpy(), v[idx].cpu().numpy()
+    fc.firecaffe_sgd_step(w, g, v, **HYPER)
+    torch.cuda.synchronize()
+    w_ref, v_ref = oracle.sgd(w0, v0, g0, **HYPER)
+    assert_bitexact(w[idx], w_ref, "w")
+    assert_bitexact(v[idx], v_ref, "v")
+    del g, w, v
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("sched,bcast", [("flat", "direct"), ("forest", "direct")])
+def test_virtual_fused_beyond_2_31_elements(sched, bcast):
+    """The fused tree at n > 2^31 on a 2-rank virtual world (~52 GB of heaps):
+    every rank's w' and owned v' bit-exact vs the oracle on sampled indices."""
+    if not _big_enough(60):
+        pytest.skip("needs ~60 GB of free device memory")
+    n, p = BIG_N, 2
+    W = _world(p, n)
+    try:
+        W.config(sched, bcast, 2)
+        grads, ws, moms = W.alloc(n), W.alloc(n), W.alloc(n)
+        ws[0].normal_(0.0, 1e-2)
+        moms[0].normal_(0.0, 1e-4)
+        for r in range(p):
+            grads[r].normal_(0.0, 1e-2)
+            if r:
+                ws[r].copy_(ws[0])
+                moms[r].copy_(moms[0])
+        gen = torch.Generator().manual_seed(32)
+        idx = torch.cat([torch.randint(0, n, (20000,), generator=gen), torch.arange(n - 9, n),
+                         torch.arange((1 << 31) - 5, (1 << 31) + 5)]).cuda()
+        G = np.stack([grads[r][idx].cpu().numpy() for r in range(p)])
+        w0, v0 = ws[0][idx].cpu().numpy(), moms[0][idx].cpu().numpy()
+        fc.firecaffe_tree_allreduce_sgd(ws[0], grads[0], moms[0], world=W, **HYPER)
+        assert W.poll() == 0
+        w_ref, v_ref = oracle.fused_step(G, w0, v0, **HYPER)
+        for r in range(p):
+            assert_bitexact(ws[r][idx], w_ref, f"w rank {r}")
+            b, e = W.owned_range(r, n)
+            own = ((idx >= b) & (idx < e)).cpu().numpy()
+            assert_bitexact(moms[r][idx].cpu().numpy()[own], v_ref[own], f"mom rank {r}")
+    finally:
+        W.close()
+        torch.cuda.empty_cache()
