@@ -19,13 +19,14 @@ namespace fc {
 
 constexpr int TREE_T = kTreeThreads;              // threads per CTA (tree schedules)
 constexpr int FLAT_T = kFlatThreads;              // threads per CTA (FLAT / PS), one CTA per SM
-// float4 per thread per operand in flight in FLAT: enough remote bytes in flight
-// (148 CTAs x 512 thr x (P-1) x U x 16 B >= 2.4 MB) at <= 128 registers
-// (measured: U = 4 best at p = 2, U = 2 at p = 4; profiles/r01_sweep_flat_unroll_*).
-// p >= 6: U = 1 — U = 2 needs more than the 128 registers a 512-thread CTA
-// allows and spills 96-140 B/thread (ptxas -v), while U = 1 still keeps
-// 148 x 512 x 5..7 x 16 B = 6-8.5 MB in flight per GPU.
-#define FLAT_UNROLL(P) ((P) <= 2 ? 4 : (P) <= 5 ? 2 : 1)
+// float4 per thread per operand in flight in FLAT (per claimed unit run of the
+// dynamic mapping): U = 2 at p = 2, U = 1 from p = 3 on.  With the dynamic
+// claims, smaller runs measured faster than round 1's U = 4 / 2 (finer claims,
+// and 148 CTAs x 512 thr x (P-1) x U x 16 B is still >= 2.4 MB of remote loads
+// in flight): p = 2 U = 2 vs 4 0-2 %, p = 4 U = 1 vs 2 0.7-2.2 % faster at
+// NiN..AlexNet sizes (profiles/r02_flat_unroll_dyn.txt, A/B twice).  U = 2 at
+// p >= 6 would exceed the 128 registers of a 512-thread CTA (spills).
+#define FLAT_UNROLL(P) ((P) <= 2 ? 2 : 1)
 constexpr int C4 = FC_CHUNK_FLOATS / 4;           // float4 per chunk (1024)
 constexpr int PER_T = C4 / TREE_T;                // float4 per thread per chunk (4)
 static_assert(C4 % TREE_T == 0, "chunk must split evenly over the CTA");
