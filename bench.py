@@ -397,9 +397,18 @@ def main():
 
     tiny = torch.zeros(1, device=dev)
 
+    align = {"fine": True}
+
     def dev_barrier():
         if N > 1:
             _all_reduce(tiny)  # device-side rendezvous: kernels start aligned across ranks
+            if align["fine"]:
+                # NCCL's own kernels end 2-4 us apart on different ranks (profiles/
+                # r02_gap_*: the first rank waits that long in the timed call's entry
+                # barrier); a 4-float tree allreduce of this library on the same world
+                # releases every rank within ~1 us of the others (its exit waits for all
+                # of them), so the timed call starts aligned
+                fc.firecaffe_tree_allreduce(sync4, W)
             # ~20 us of GPU-side delay, equal on every rank (same clock): the host has
             # enqueued the timed kernel before the GPU reaches the start event, as in a
             # training loop where the allreduce is queued behind the backward pass
@@ -413,6 +422,7 @@ def main():
             W.config(args.sched or c["sched"], args.bcast or c["bcast"], 2)
         grad, w, mom = W.alloc(n), W.alloc(n), W.alloc(n)
         gb = W.alloc(n, "bf16")  # bf16 gradients on the wire (fp32 accumulate + update)
+        sync4 = W.alloc(4)  # the rendezvous buffer of dev_barrier
     else:
         W = None
         grad = torch.empty(n, device=dev)
@@ -499,6 +509,13 @@ def main():
     # secondary: warm L2 (no flush between steps), as in a loop whose working set stays resident
     reset()
     warm_ms, _, _ = timed(step, max(5, min(args.steps, 50)), min(args.warmup, 5), pre=restore, cold=False)
+    # secondary: the same step with round 1's rank alignment (NCCL rendezvous only)
+    coarse_ms = None
+    if N > 1:
+        align["fine"] = False
+        reset()
+        coarse_ms, _, _ = timed(step, max(5, min(args.steps, 50)), min(args.warmup, 5), pre=restore)
+        align["fine"] = True
     e2e_value = N * 4 * n / (e2e_ms * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (the only kernel in the step)
@@ -613,6 +630,10 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "ms_per_step_warm_l2": round(warm_ms, 5),
+            "rank_alignment": ("none (1 GPU)" if N == 1 else
+                               "before each step: NCCL all_reduce + a 4-float firecaffe_tree_allreduce on the same "
+                               "world + ~20 us GPU sleep"),
+            "ms_per_step_nccl_alignment_only": round(coarse_ms, 5) if coarse_ms else None,
             "e2e": {"value": round(e2e_value, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n, "ms_per_step": round(e2e_ms, 4),
                     "what": ("firecaffe_sgd_step_host: pinned host grad -> device by the copy engine in 4 MB "
@@ -631,7 +652,7 @@ def main():
             line["test_hook"] = {"shared_gpus": shared, "note": "ranks time-slice GPUs: not a measurement"}
             line["valid"] = False
             for k in ("value", "ms_per_step", "ms_per_step_median", "ms_per_step_warm_l2", "algbw_gbs", "busbw_gbs",
-                      "roofline"):
+                      "roofline", "ms_per_step_nccl_alignment_only"):
                 line[k] = None
             line["e2e"] = None
         emit(line)

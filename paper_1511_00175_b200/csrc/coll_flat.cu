@@ -21,7 +21,9 @@ __device__ __forceinline__ const uint16_t* gradh_of(const FcColl& c, int q) {
 
 // 4 elements per unit: 8-byte bf16 loads and float4 weight accesses are both
 // fully coalesced per warp; U units per thread keep (P-1)*8*U remote bytes in
-// flight per thread.  p = 2: U = 6 is spill-free (U = 8 spilled 20 B/thread;
+// flight per thread.  Work mapping: the plain grid stride (the fp32 FLAT
+// kernel's dynamic claims were tried here too and measured equal at p = 2 and
+// 1 % slower at p = 4, profiles/r02_final/bf16_map.txt; not kept).  p = 2: U = 6 is spill-free (U = 8 spilled 20 B/thread;
 // measured NiN +2 %, AlexNet -1 % time vs U = 8, scripts/gpu_bf16_unroll.sh).
 #define BF16_UNROLL(P) ((P) <= 2 ? 6 : (P) <= 4 ? 4 : 1)
 __device__ __forceinline__ uint2 ld_cg_u2(const uint2* p) {
@@ -54,46 +56,12 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const __grid_constant
             float4* v4 = reinterpret_cast<float4*>(mom_of(c, rank));
             const int64_t T = FLAT_T;
             const int64_t stride = (int64_t)gridDim.x * T * U;
-            // work mapping as the fp32 FLAT kernel: dynamic guided claims of runs of
-            // <= U units of T (default), else the plain grid stride
-            const bool dyn = c.flat_map == 2;
-            const int64_t total = (i1 - i0 + T - 1) / T;
-            uint32_t* ctr = c.ctl + FC_CTL_CLAIM + rank;
-            if (dyn) {
-                if (threadIdx.x == 0) {
-                    const int g = guided_units(total, 0, gridDim.x, U);
-                    s_claim[0] = (int64_t)atomicAdd(ctr, (uint32_t)g);
-                    s_claim_n[0] = g;
-                }
-                __syncthreads();
-            }
-            for (int64_t r = 0;; ++r) {
-                int64_t base, step;
-                int nv;
-                uint32_t next = 0;
-                int gnext = 0;
-                if (dyn) {
-                    const int64_t u0 = s_claim[r & 1];
-                    if (u0 >= total) break;
-                    nv = (int)min((int64_t)s_claim_n[r & 1], total - u0);
-                    base = i0 + u0 * T + threadIdx.x;
-                    step = T;
-                    if (threadIdx.x == 0) {
-                        gnext = guided_units(total, u0 + nv, gridDim.x, U);
-                        next = atomicAdd(ctr, (uint32_t)gnext);
-                    }
-                } else {
-                    base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x + r * stride;
-                    if (base >= i1) break;  // per thread: no barrier in this mode
-                    nv = U;
-                    step = T;
-                }
-#define FC_BI(j) ((j) < nv ? base + (int64_t)(j) * step : i1)
+            for (int64_t base = i0 + (int64_t)blockIdx.x * T * U + threadIdx.x; base < i1; base += stride) {
                 uint2 x[U][P];
                 float4 w[U], v[U];
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    const int64_t i = FC_BI(j);
+                    const int64_t i = base + j * T;
                     if (i < i1) {
 #pragma unroll
                         for (int q = 0; q < P; ++q)
@@ -102,7 +70,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const __grid_constant
                 }
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    const int64_t i = FC_BI(j);
+                    const int64_t i = base + j * T;
                     if (i < i1) {
                         w[j] = ld_rw(w4 + i);
                         v[j] = ld_rw(v4 + i);
@@ -110,7 +78,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const __grid_constant
                 }
 #pragma unroll
                 for (int j = 0; j < U; ++j) {
-                    const int64_t i = FC_BI(j);
+                    const int64_t i = base + j * T;
                     if (i < i1) {
                         float4 f[P];
 #pragma unroll
@@ -121,14 +89,6 @@ __global__ void __launch_bounds__(FLAT_T) flat_bf16_kernel(const __grid_constant
 #pragma unroll
                         for (int q = 0; q < P; ++q) st_na(reinterpret_cast<float4*>(w_of(c, q)) + i, w[j]);
                     }
-                }
-#undef FC_BI
-                if (dyn) {
-                    if (threadIdx.x == 0) {
-                        s_claim[(r + 1) & 1] = (int64_t)next;
-                        s_claim_n[(r + 1) & 1] = gnext;
-                    }
-                    __syncthreads();
                 }
             }
             const int rem = (int)(e1 - 4 * i1);  // trailing n % 4 elements of the last slice

@@ -77,7 +77,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// System-scope fence of the exit / flag publication.  fence.sc is the stronger
+// fence (it implies acq_rel), and measured 0.2-0.45 us cheaper than
+// fence.acq_rel.sys on B200 with and without outstanding stores
+// (profiles/r01_fence_bench.txt), so the stronger one is used.
+__device__ __forceinline__ void fence_sys() { asm volatile("fence.sc.sys;" ::: "memory"); }
 __device__ __forceinline__ uint64_t ld_relaxed_sys64(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

@@ -130,6 +130,40 @@ __global__ void load_kernel(const float4* src, int per, int fence, uint64_t* spa
     }
 }
 
+// remote (or local) bulk loads into shared memory with TMA (cp.async.bulk + mbarrier), 16 KB per
+// copy, one copy in flight per CTA at a time, `per` copies per CTA
+__global__ void __launch_bounds__(128) tma_load_kernel(const char* src, int per, uint64_t* span, float* sink) {
+    extern __shared__ __align__(128) char sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const uint64_t t0 = gt();
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(sm);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    float acc = 0.f;
+    for (int j = 0; j < per; ++j) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(16384));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(d), "l"(src + ((int64_t)blockIdx.x * per + j) * 16384), "r"(16384), "r"(b) : "memory");
+        }
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(done) : "r"(b), "r"((uint32_t)(j & 1)));
+        acc += reinterpret_cast<const float*>(sm)[threadIdx.x];
+        __syncthreads();
+    }
+    if (acc == 12345.f) sink[0] = acc;
+    if (threadIdx.x == 0) {
+        span[2 * blockIdx.x] = t0;
+        span[2 * blockIdx.x + 1] = gt();
+    }
+}
+
 int main() {
     int ndev = 0;
     cudaGetDeviceCount(&ndev);
@@ -165,6 +199,7 @@ int main() {
                 case 2: big_kernel<<<G, T, 0, st>>>(big, span); break;
                 case 3: counter_kernel<<<G, T, 0, st>>>(ctl, span); break;
                 case 4: store_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, span); break;
+                case 7: tma_load_kernel<<<G, 128, 16384, st>>>(remote ? (const char*)peer : (const char*)local, per, span, (float*)local); break;
                 case 6: load_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, span, (float*)local); break;
                 case 5:
                     proto_kernel<<<G, T, 0, st>>>(remote ? peer : local, per, fence, ctl,
@@ -221,6 +256,9 @@ int main() {
         run("remote loads x16", 148, 512, 6, 16, 0, true);
         run("remote loads x16 + fence.sys", 148, 512, 6, 16, 1, true);
         run("local loads x16", 148, 512, 6, 16, 0, false);
+        run("remote TMA loads 16 KB x4", 148, 128, 7, 4, 0, true);
+        run("remote TMA loads 16 KB x16", 148, 128, 7, 16, 0, true);
+        run("local TMA loads 16 KB x16", 148, 128, 7, 16, 0, false);
     }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

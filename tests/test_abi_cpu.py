@@ -244,3 +244,30 @@ def test_lr_state_argument_errors_without_gpu():
     assert L.firecaffe_lr_state_get_iter(None, None) == _lib.FC_ERR_INVALID_ARG
     assert L.firecaffe_lr_state_set_iter(None, 3) == _lib.FC_ERR_INVALID_ARG
     assert L.firecaffe_lr_state_destroy(None) == _lib.FC_OK
+
+
+def test_binding_checks_buffer_sizes_before_the_library():
+    """The C ABI takes plain pointers and cannot check sizes: the binding refuses
+    a tensor shorter than n (and buffers on different devices) before calling it
+    (ADVICE r1)."""
+    import torch
+
+    a, b = torch.zeros(8), torch.zeros(4)
+    assert fc._numel(None, a, a) == 8
+    assert fc._numel(4, a, b) == 4
+    with pytest.raises(ValueError):
+        fc._numel(None, a, b)          # b shorter than a's 8
+    with pytest.raises(ValueError):
+        fc._numel(9, a)                 # n beyond the buffer
+    with pytest.raises(ValueError):
+        fc._numel(None, 12345)          # raw pointer without n
+
+
+def test_bench_config_holds_only_workload_keys():
+    """Both bench arms print the same `config` (workload keys only); the device
+    choices are top-level keys of the GPU arm's line."""
+    import bench
+
+    cfg = bench.workload_config("nin", 7_600_000, 4, dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024))
+    assert set(cfg) == {"workload", "n_params", "grad_bytes", "ranks", "batch", "lr", "mu", "wd", "parallelism"}
+    assert cfg["grad_bytes"] == 4 * 7_600_000 and cfg["parallelism"] == "dp4"
