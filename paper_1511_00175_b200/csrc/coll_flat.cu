@@ -23,7 +23,7 @@ __device__ __forceinline__ const uint16_t* gradh_of(const FcColl& c, int q) {
 // fully coalesced per warp; U units per thread keep (P-1)*8*U remote bytes in
 // flight per thread.  Work mapping: the plain grid stride (the fp32 FLAT
 // kernel's dynamic claims were tried here too and measured equal at p = 2 and
-// 1 % slower at p = 4, profiles/r02_final/bf16_map.txt; not kept).  p = 2: U = 6 is spill-free (U = 8 spilled 20 B/thread;
+// 1 % slower at p = 4, profiles/r02_bf16_dyn_vs_stride.txt; not kept).  p = 2: U = 6 is spill-free (U = 8 spilled 20 B/thread;
 // measured NiN +2 %, AlexNet -1 % time vs U = 8, scripts/gpu_bf16_unroll.sh).
 #define BF16_UNROLL(P) ((P) <= 2 ? 6 : (P) <= 4 ? 4 : 1)
 __device__ __forceinline__ uint2 ld_cg_u2(const uint2* p) {

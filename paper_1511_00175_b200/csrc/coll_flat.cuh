@@ -138,10 +138,10 @@ __device__ __forceinline__ void flat_row(const FcColl& c, int rank, int64_t rb, 
 // behind the row.  All CTAs still sweep the slice front to back together.
 __shared__ int64_t s_claim[2];
 __shared__ int s_claim_n[2];
-__device__ __forceinline__ int guided_units(int64_t total, int64_t next, int G, int U) {
+__device__ __forceinline__ int guided_units(int64_t total, int64_t next, int G, int gmax) {
     const int64_t rem = total - next;
     int64_t g = rem / (2 * (int64_t)G);
-    return (int)(g < 1 ? 1 : g > U ? U : g);
+    return (int)(g < 1 ? 1 : g > gmax ? gmax : g);
 }
 
 template <int P, int K, int U>
@@ -188,12 +188,20 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
             const int64_t rows = stride ? (M + GT * U - 1) / (GT * U) : (nslab + U - 1) / U;
             const int64_t me = stride ? (int64_t)blockIdx.x * T * U + threadIdx.x
                                       : (int64_t)blockIdx.x * T + threadIdx.x;
-            const int64_t total = (M + T - 1) / T;  // dyn: units of T float4
+            // dyn: the counter counts units of T float4; a claim of g units covers
+            // g*T consecutive float4 and thread t takes base + t + j*T (j < g).
+            // (Quarter units -- short last rows of a quarter of the threads -- were
+            // built and measured: the CTAs then end within ~3 us instead of ~9 us at
+            // p = 4, but the last CTA ends no sooner (the link is saturated to the
+            // end) and p = 2 got 3 % slower; profiles/r02_flat_quarter_claims.txt.)
+            constexpr int QU = 1;
+            const int64_t TQ = T / QU;
+            const int64_t total = (M + TQ - 1) / TQ;
             const int G = gridDim.x;
             uint32_t* ctr = c.ctl + FC_CTL_CLAIM + rank;
             if (dyn) {
                 if (threadIdx.x == 0) {
-                    const int g = guided_units(total, 0, G, U);
+                    const int g = guided_units(total, 0, G, QU * U);
                     s_claim[0] = (int64_t)atomicAdd(ctr, (uint32_t)g);
                     s_claim_n[0] = g;
                 }
@@ -201,19 +209,21 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
             }
             int64_t s0 = 0;
             for (int64_t r = 0;; ++r) {
-                // element j of this thread in row r: rb + j * step, for j < nv (and < ce)
-                int64_t rb, step;
+                // element j of this thread in row r: rb + j * step, for j < nv (and < lim)
+                int64_t rb, step, lim = ce;
                 int nv;
                 uint32_t next = 0;
                 int gnext = 0;
                 if (dyn) {
-                    const int64_t u0 = s_claim[r & 1];
-                    if (u0 >= total) break;
-                    nv = (int)min((int64_t)s_claim_n[r & 1], total - u0);
-                    rb = i0 + u0 * T + threadIdx.x;
+                    const int64_t q0 = s_claim[r & 1];
+                    if (q0 >= total) break;
+                    const int64_t g = min((int64_t)s_claim_n[r & 1], total - q0);
+                    rb = i0 + q0 * TQ + threadIdx.x;
                     step = T;
+                    nv = U;
+                    lim = min(ce, i0 + (q0 + g) * TQ);
                     if (threadIdx.x == 0) {  // the next claim; its result is needed only after this row
-                        gnext = guided_units(total, u0 + nv, G, U);
+                        gnext = guided_units(total, q0 + g, G, QU * U);
                         next = atomicAdd(ctr, (uint32_t)gnext);
                     }
                 } else {
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
                     step = stride ? T : GT;
                     s0 = s1;
                 }
-                flat_row<P, K, U>(c, rank, rb, nv, step, ce, fused, pull);
+                flat_row<P, K, U>(c, rank, rb, nv, step, lim, fused, pull);
                 if (dyn) {
                     if (threadIdx.x == 0) {
                         s_claim[(r + 1) & 1] = (int64_t)next;

@@ -979,7 +979,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_FLAT_UNROLL": "1"}, {"FC_FLAT_UNROLL": "2"}, {"FC_FLAT_UNROLL": "4"},  # every FLAT unroll build
     {"FC_EXIT": "push"}, {"FC_EXIT": "cta"},            # the other exit protocols (coll_common.cuh)
     {"FC_FLAT_MAP": "stride"},                          # the plain grid-stride FLAT work mapping
-    {"FC_FLAT_MAP": "dyn"}, {"FC_FLAT_MAP": "balanced"},  # dynamic claims / static balanced rows
+    {"FC_FLAT_MAP": "balanced"},                        # the static balanced rows (round 1's default)
 ])
 def test_every_kernel_build_bitexact(knobs):
     """The dispatcher picks among several builds of each executor (register
