@@ -197,8 +197,7 @@ static __device__ __forceinline__ void exit_rank(const FcColl& c, int rank, int 
         const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
         const bool poll = c.rank_exit == 2;
         if (t == 0) {
-            __threadfence();
-            fence_sys();
+            fence_sys();  // (sc.sys subsumes the gpu-scope acquire fence after the counter)
             if (poll) {
                 st_relaxed_sys64(bar_flag(c, rank, 1, cta_slot, rank), stamp);
             } else {
