@@ -164,6 +164,17 @@ static int flat_map() {
     return m;
 }
 
+// FLAT dynamic mapping: issue each CTA's first claim before the entry barrier
+// (default) or after it (FC_FLAT_PRECLAIM=0, A/B only).  Value-neutral.
+static int flat_preclaim() {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("FC_FLAT_PRECLAIM");
+        m = (e && strcmp(e, "0") == 0) ? 0 : 1;
+    }
+    return m;
+}
+
 extern "C" {
 
 const char* firecaffe_version(void) { return FC_VERSION_STR; }
@@ -538,6 +549,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.win_k = win_k;
     c.win_s = win_s;
     c.flat_map = flat_map();
+    c.preclaim = flat_preclaim();
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;

@@ -151,14 +151,27 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
     const bool dyn = c.flat_map == 2 && !pull;  // pull pairs elements with the peer CTA's: static only
     epoch_begin(c);
     trace(c, 0);
+    const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
+    int64_t c0, c1;
+    owned_chunks(rank, P, nch, c.op == FC_OP_PS, &c0, &c1);
+    const int64_t e0 = c0 * FC_CHUNK_FLOATS;
+    const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
+    // dyn: the CTA's first work claim touches only this rank's counter, so it is
+    // issued BEFORE the entry barrier (by a thread the barrier does not use) and
+    // its latency hides behind the barrier's stamp round trip
+    constexpr int CLAIM_T = 32;
+    uint32_t first_claim = 0;
+    int first_g = 0;
+    const bool pre = c.preclaim != 0;
+    if (dyn && pre && e1 > e0 && threadIdx.x == CLAIM_T) {
+        int64_t a = e0 / 4, b = e1 / 4;
+        if (c.win_s > 1) window_range(e0 / 4, e1 / 4, c.win_k, c.win_s, &a, &b);
+        first_g = guided_units((b - a + FLAT_T - 1) / FLAT_T, 0, gridDim.x, U);
+        first_claim = atomicAdd(c.ctl + FC_CTL_CLAIM + rank, (uint32_t)first_g);
+    }
     const bool ok = cta_barrier(c, rank, 0);
     trace(c, 1);
     if (ok) {
-        const int64_t nch = (c.n + FC_CHUNK_FLOATS - 1) / FC_CHUNK_FLOATS;
-        int64_t c0, c1;
-        owned_chunks(rank, P, nch, c.op == FC_OP_PS, &c0, &c1);
-        const int64_t e0 = c0 * FC_CHUNK_FLOATS;
-        const int64_t e1 = min(c1 * FC_CHUNK_FLOATS, c.n);
         const bool fused = c.op == FC_OP_ALLREDUCE_SGD;
         if (e1 > e0) {
             // push broadcast: results go to every rank's buffer now; pull broadcast:
@@ -200,10 +213,13 @@ __global__ void __launch_bounds__(FLAT_T) flat_kernel(const __grid_constant__ Fc
             const int G = gridDim.x;
             uint32_t* ctr = c.ctl + FC_CTL_CLAIM + rank;
             if (dyn) {
-                if (threadIdx.x == 0) {
-                    const int g = guided_units(total, 0, G, QU * U);
-                    s_claim[0] = (int64_t)atomicAdd(ctr, (uint32_t)g);
-                    s_claim_n[0] = g;
+                if (!pre && threadIdx.x == CLAIM_T) {  // FC_FLAT_PRECLAIM=0: claim after the barrier
+                    first_g = guided_units(total, 0, G, QU * U);
+                    first_claim = atomicAdd(ctr, (uint32_t)first_g);
+                }
+                if (threadIdx.x == CLAIM_T) {
+                    s_claim[0] = (int64_t)first_claim;
+                    s_claim_n[0] = first_g;
                 }
                 __syncthreads();
             }

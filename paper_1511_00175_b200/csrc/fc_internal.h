@@ -114,6 +114,7 @@ struct FcColl {
     int rank_exit;     // 1: rank-level exit (one sys fence per GPU), 0: per-CTA exit barrier
     int win_k, win_s;  // FLAT push only: process window win_k of win_s of the owned slice (win_s <= 1: all)
     int flat_map;      // FLAT work mapping: 0 = balanced slab rows, 1 = plain grid stride, 2 = dynamic claims
+    int preclaim;      // FLAT dyn: 1 = the first claim is issued before the entry barrier (default)
 };
 
 #define FC_TRACE_SLOTS 4

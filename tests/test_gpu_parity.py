@@ -980,6 +980,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_EXIT": "push"}, {"FC_EXIT": "cta"},            # the other exit protocols (coll_common.cuh)
     {"FC_FLAT_MAP": "stride"},                          # the plain grid-stride FLAT work mapping
     {"FC_FLAT_MAP": "balanced"},                        # the static balanced rows (round 1's default)
+    {"FC_FLAT_PRECLAIM": "0"},                          # dynamic claims: first claim after the entry barrier
 ])
 def test_every_kernel_build_bitexact(knobs):
     """The dispatcher picks among several builds of each executor (register
