@@ -201,6 +201,38 @@ def main():
             fails.append(f"host entry segments w n={n}")
         if not np.array_equal(bits(mom[b:e]), vs_ref[b:e].view(np.uint32)):
             fails.append(f"host entry segments mom n={n}")
+    # CUDA-graph capture on a real world: every rank captures (gradient refresh +
+    # fused call) once and replays it; the call's epoch, work-claim counters and
+    # schedule state live on the device, so each replay is a new collective and
+    # K replays == K oracle steps, bit for bit
+    n = sizes[-1]
+    W.config("flat", "direct", 2)
+    g_src = g_all[rank].to(dev)
+    w0g, v0g = fc_inputs.weights(n, seed=81), fc_inputs.momentum(n, seed=82)
+    w[:n].copy_(w0g)
+    mom[:n].copy_(v0g)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        grad[:n].copy_(g_src)
+        fc.firecaffe_tree_allreduce_sgd(w, grad, mom, world=W, n=n, **HP)
+    torch.cuda.synchronize()
+    dist.barrier()
+    K = 3
+    for _ in range(K):
+        graph.replay()
+    torch.cuda.synchronize()
+    S_g = oracle.tree_sum(g_all.numpy(), 2)
+    wr, vr = w0g.numpy(), v0g.numpy()
+    for _ in range(K):
+        wr, vr = oracle.sgd(wr, vr, S_g, **HP)
+    if not np.array_equal(bits(w[:n]), wr.view(np.uint32)):
+        fails.append("graph replay w")
+    b, e = W.owned_range(rank, n)
+    if not np.array_equal(bits(mom[b:e]), vr[b:e].view(np.uint32)):
+        fails.append("graph replay mom")
+    del graph
     # back-to-back fused steps across real GPUs, no host synchronisation between
     # them (each rank refreshes its own gradient with a stream-ordered copy)
     n = sizes[-1]
