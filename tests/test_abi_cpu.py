@@ -271,3 +271,24 @@ def test_bench_config_holds_only_workload_keys():
     cfg = bench.workload_config("nin", 7_600_000, 4, dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024))
     assert set(cfg) == {"workload", "n_params", "grad_bytes", "ranks", "batch", "lr", "mu", "wd", "parallelism"}
     assert cfg["grad_bytes"] == 4 * 7_600_000 and cfg["parallelism"] == "dp4"
+
+
+def test_reference_arm_runs_on_cpu():
+    """`bench.py --impl reference` (the tier's reference arm: the oracle's
+    OpenMP build on the host cores) needs no GPU: one step prints the contract's
+    JSON line with the same workload config as the GPU arm."""
+    import json
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GB/s"
+    import bench
+    assert d["config"] == bench.workload_config("nin", 7_600_000, 1, dict(lr=0.04, mu=0.9, wd=5e-4, batch=1024))
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["cpu_baseline"]["cores"] >= 1
