@@ -124,3 +124,33 @@ def test_bench_eight_ranks_on_shared_gpus():
     for key in ("forest/direct_ms", "forest/tree_ms", "flat/direct_ms", "single_root/tree_ms",
                 "single_root/direct_ms", "ps+sgd_ms", "flat_bf16_wire_ms"):
         assert d["baselines_ms_per_step"][key] > 0, key
+
+
+def test_bench_two_ranks_on_one_gpu():
+    """bench.py's N > 1 code path end to end on a ONE-GPU box (the driver's
+    round-end GPU tests run on one GPU): two ranks share GPU 0 through the
+    FC_BENCH_SHARED_GPUS test hook (gloo group, CUDA-IPC heaps).  The line is
+    marked invalid (time-sliced ranks: no timing is reported), but the full-size
+    NiN step must be bit-exact on the sampled indices on both ranks, and every
+    executor, the PS baseline and the bf16 wire bit-exact (parity.executors)."""
+    import json
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, FC_BENCH_SHARED_GPUS="1", OMP_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29629", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out[-4000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["valid"] is False and d["value"] is None
+    assert d["parity"]["bitexact_sampled"] and d["parity"]["ranks_identical_digest"], d["parity"]
+    assert d["parity"]["device_status"] == 0
+    ex = d["parity"]["executors"]
+    for key in ("flat/direct", "flat/pull", "forest/direct", "forest/tree", "single_root/tree",
+                "single_root/direct", "ps+sgd", "flat_bf16_wire"):
+        assert ex[key] is True, (key, ex)
