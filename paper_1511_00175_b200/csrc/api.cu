@@ -175,6 +175,21 @@ static int flat_preclaim() {
     return m;
 }
 
+// Rank-level exit: the CTAs that are not last issue a sys-scope fence after
+// arriving (default) or leave at once (FC_CLEAN_EXIT=0, round 1's exit).
+// Measured (profiles/r02_exit_clean.txt, A/B three times): the kernel's
+// completion drops from ~9 to ~6 us (an empty kernel's), the span grows by
+// 1.2-1.6 us (the concurrent fences), net NiN p = 4 -2.0 us, p = 2 -0.6 us,
+// GoogLeNet / AlexNet -1.0..-1.6 us.  Value-neutral.
+static int clean_exit() {
+    static int m = -1;
+    if (m < 0) {
+        const char* e = getenv("FC_CLEAN_EXIT");
+        m = (e && strcmp(e, "0") == 0) ? 0 : 1;
+    }
+    return m;
+}
+
 extern "C" {
 
 const char* firecaffe_version(void) { return FC_VERSION_STR; }
@@ -550,6 +565,7 @@ static fc_status collective(fc_world* w, int op, float* wt, float* grad, float* 
     c.win_s = win_s;
     c.flat_map = flat_map();
     c.preclaim = flat_preclaim();
+    c.clean_exit = clean_exit();
     c.owner_single_root = w->sched == FC_SCHED_SINGLE_ROOT ? 1 : 0;
     c.timeout_ns = w->timeout_ns;
     c.status = w->d_status;

@@ -192,7 +192,18 @@ static __device__ __forceinline__ void exit_rank(const FcColl& c, int rank, int 
         s_last = atomicAdd(c.ctl + 1, 1u) + 1u == total;
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last) {
+        // c.clean_exit (default): a CTA that is not the last one fences at system
+        // scope AFTER arriving -- off the last CTA's critical path, concurrent with
+        // its remaining work -- so that when the grid ends only the last CTA's SM
+        // has peer accesses not yet made system-visible, and the end-of-grid flush
+        // is short: completion ~6 instead of ~9 us, net 0.6-2 us per call
+        // (scripts/gap_bench.cu, profiles/r02_gap_bench.txt, r02_exit_clean.txt).
+        // Not needed for correctness (the last CTA's fence covers every CTA's
+        // stores through the counter).
+        if (c.clean_exit && c.rank >= 0 && t == 0) fence_sys();
+        return;
+    }
     if (c.rank >= 0) {
         const uint64_t stamp = (uint64_t)s_epoch | ((uint64_t)c.sig << 32);
         const bool poll = c.rank_exit == 2;

@@ -115,6 +115,7 @@ struct FcColl {
     int win_k, win_s;  // FLAT push only: process window win_k of win_s of the owned slice (win_s <= 1: all)
     int flat_map;      // FLAT work mapping: 0 = balanced slab rows, 1 = plain grid stride, 2 = dynamic claims
     int preclaim;      // FLAT dyn: 1 = the first claim is issued before the entry barrier (default)
+    int clean_exit;    // rank-level exit: 1 = non-last CTAs fence at sys scope after arriving (default)
 };
 
 #define FC_TRACE_SLOTS 4

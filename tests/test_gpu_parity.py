@@ -981,6 +981,7 @@ def test_virtual_rejects_non_symmetric_buffers():
     {"FC_FLAT_MAP": "stride"},                          # the plain grid-stride FLAT work mapping
     {"FC_FLAT_MAP": "balanced"},                        # the static balanced rows (round 1's default)
     {"FC_FLAT_PRECLAIM": "0"},                          # dynamic claims: first claim after the entry barrier
+    {"FC_CLEAN_EXIT": "0"},                             # rank-level exit without the non-last CTAs' sys fences
 ])
 def test_every_kernel_build_bitexact(knobs):
     """The dispatcher picks among several builds of each executor (register
